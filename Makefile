@@ -1,0 +1,35 @@
+# Build of the product library and the CPU checkers.
+#
+#   paper_1805_02867_b200/libosmx_b200.so   the sm_100a kernels + C-ABI
+#   oracle/_build, oracle/_ref              test infrastructure (oracle/Makefile)
+#
+# nvcc cross-compiles sm_100a without a GPU.  No fast-math (SURVEY.md sec.7
+# risk 3): outputs keep IEEE expf / reciprocal and denormals.
+
+NVCC ?= nvcc
+ARCH = -gencode arch=compute_100a,code=sm_100a
+NVFLAGS = $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O2,-Wall -Xptxas -v -diag-suppress 177 \
+          --expt-relaxed-constexpr -Iinclude
+SRC_DIR = paper_1805_02867_b200/csrc
+SRCS = $(wildcard $(SRC_DIR)/*.cu)
+HDRS = $(wildcard $(SRC_DIR)/*.cuh) $(SRC_DIR)/internal.hpp include/osmx_b200.h
+OBJS = $(patsubst $(SRC_DIR)/%.cu,build/%.o,$(SRCS))
+LIB = paper_1805_02867_b200/libosmx_b200.so
+
+all: $(LIB) oracle
+
+build/%.o: $(SRC_DIR)/%.cu $(HDRS)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; false)
+
+$(LIB): $(OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart
+
+oracle:
+	$(MAKE) -s -C oracle
+
+clean:
+	rm -rf build $(LIB)
+	$(MAKE) -s -C oracle clean
+
+.PHONY: all oracle clean

@@ -1,0 +1,170 @@
+/*
+ * osmx_b200.h -- C-ABI of the B200 (sm_100a) implementation of the online-
+ * normalizer softmax and fused softmax+TopK (arXiv 1805.02867).
+ *
+ * This is the drop-in boundary for the reference library `osmx`
+ * (/root/reference/proj).  The reference has no FFI: its seam is the C++
+ * header API.  Each entry point below names the
+ * reference interface it replaces; include/osmx/b200.hpp re-exposes them
+ * under the reference's own C++ signatures and exception types.
+ *
+ * Conventions
+ *   - extern "C", plain pointers and sizes; no C++ or torch types.
+ *   - Device-pointer entry points are stream-ordered, allocate nothing, and
+ *     return argument errors synchronously.  `stream` is a cudaStream_t
+ *     (NULL = legacy default stream).
+ *   - Rows are row-major with a leading dimension in ELEMENTS (ld >= V).
+ *   - The workspace `ws` is caller-owned device memory of at least
+ *     osmx_workspace_bytes(...) bytes, zero-initialised once with
+ *     osmx_workspace_init.  Non-finite input rows are reported through it
+ *     (osmx_check_status), like the reference's non_finite_error
+ *     (error.hpp:13-15); their outputs are unspecified.
+ *   - Host-buffer entry points (suffix _host) mirror the reference's
+ *     span-in / vector-out functions for a whole batch: they copy in, run,
+ *     copy out and synchronise, and report non-finite input synchronously.
+ */
+#ifndef OSMX_B200_H
+#define OSMX_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes.  1..4 are the reference's four exception types
+ * (error.hpp:8-25), in that order. */
+typedef enum {
+  OSMX_OK = 0,
+  OSMX_ERR_EMPTY = 1,         /* empty_input_error   error.hpp:8-10  */
+  OSMX_ERR_NON_FINITE = 2,    /* non_finite_error    error.hpp:13-15 */
+  OSMX_ERR_INVALID_K = 3,     /* invalid_k_error     error.hpp:18-20 */
+  OSMX_ERR_INVALID_CHUNK = 4, /* invalid_chunk_error error.hpp:23-25 */
+  OSMX_ERR_INVALID_ARG = 5,   /* null pointer, ld < V, bad enum, ws too small */
+  OSMX_ERR_CUDA = 6,          /* a CUDA runtime error (see osmx_last_cuda_error) */
+  OSMX_ERR_UNSUPPORTED = 7    /* k above OSMX_MAX_K on the device path */
+} osmx_status;
+
+/* Algorithm ids: the reference's `algorithm` enum order (counting.hpp:17-24)
+ * plus the unfused online->TopK pipeline the north star compares against. */
+typedef enum {
+  OSMX_NAIVE_SOFTMAX = 0,               /* naive_softmax           softmax.hpp:17 */
+  OSMX_SAFE_SOFTMAX = 1,                /* safe_softmax            softmax.hpp:22 */
+  OSMX_ONLINE_SOFTMAX = 2,              /* online_softmax          softmax.hpp:28 */
+  OSMX_SAFE_SOFTMAX_UNFUSED_TOPK = 3,   /* safe_softmax_then_topk  topk.hpp:58 */
+  OSMX_SAFE_SOFTMAX_FUSED_TOPK = 4,     /* safe_softmax_fused_topk topk.hpp:63 */
+  OSMX_ONLINE_SOFTMAX_FUSED_TOPK = 5,   /* online_softmax_topk     topk.hpp:68 */
+  OSMX_ONLINE_SOFTMAX_UNFUSED_TOPK = 6  /* online_softmax then topk_of (new) */
+} osmx_algorithm;
+
+#define OSMX_MAX_K 32
+#define OSMX_VERSION 100
+
+int osmx_version(void);
+const char* osmx_status_string(osmx_status s);
+/* The last CUDA error string seen by this thread (empty if none). */
+const char* osmx_last_cuda_error(void);
+
+/* ---------------------------------------------------------- workspace -- */
+
+/* Bytes of workspace for one call of `alg` on rows x V (k for top-K algs;
+ * alg 7 = osmx_topk, 8 = osmx_normalizer, 9 = osmx_slice_record).
+ * Always >= 128 (the status header). */
+size_t osmx_workspace_bytes(int alg, int64_t rows, int64_t V, int32_t k);
+osmx_status osmx_workspace_init(void* ws, size_t ws_bytes, void* stream);
+/* Synchronises `stream`, reads the non-finite flag the kernels set since the
+ * last check, and clears it.  *first_bad_row = -1 when every row was finite,
+ * else the lowest row index that held a NaN/inf (then returns
+ * OSMX_ERR_NON_FINITE). */
+osmx_status osmx_check_status(void* ws, void* stream, int64_t* first_bad_row);
+
+/* ------------------------------------------------- batched, device ptrs -- */
+
+/* Softmax of every row.  alg in {NAIVE, SAFE, ONLINE}_SOFTMAX.
+ * Replaces naive_softmax / safe_softmax / online_softmax (softmax.hpp:17-28,
+ * softmax.cpp:19-29) applied to each row; y is caller-owned (the reference
+ * returns a fresh std::vector, softmax.cpp:12). */
+osmx_status osmx_softmax(int alg, const float* x, int64_t ldx, float* y, int64_t ldy, int64_t rows,
+                         int64_t V, void* ws, size_t ws_bytes, void* stream);
+
+/* Top-K of every row's softmax: vals/idx are rows x k (row-major).
+ * alg in {SAFE_SOFTMAX_UNFUSED_TOPK, SAFE_SOFTMAX_FUSED_TOPK,
+ * ONLINE_SOFTMAX_FUSED_TOPK, ONLINE_SOFTMAX_UNFUSED_TOPK}.
+ * Replaces safe_softmax_then_topk / safe_softmax_fused_topk /
+ * online_softmax_topk (topk.hpp:58-68, topk.cpp:30-55). */
+osmx_status osmx_softmax_topk(int alg, const float* x, int64_t ldx, int64_t rows, int64_t V,
+                              int32_t k, float* vals, int64_t* idx, void* ws, size_t ws_bytes,
+                              void* stream);
+
+/* Top-K of arbitrary values per row.  Replaces topk_of (topk.hpp:54,
+ * topk.cpp:20-28). */
+osmx_status osmx_topk(const float* v, int64_t ld, int64_t rows, int64_t V, int32_t k, float* vals,
+                      int64_t* idx, void* ws, size_t ws_bytes, void* stream);
+
+/* (m, d) of every row.  Replaces run_normalizer<float> /
+ * run_normalizer_chunked<float> (normalizer.hpp:61-85).  chunk = 0 selects
+ * the sequential contract; chunk > 0 only validates (>= 1 required by the
+ * reference, :75-76): the device reduction order is the CTA tree, which the
+ * reference's tests pin as equivalent (test_normalizer.cpp:229-262). */
+osmx_status osmx_normalizer(const float* x, int64_t ldx, int64_t rows, int64_t V, int64_t chunk,
+                            float* m, float* d, void* ws, size_t ws_bytes, void* stream);
+
+/* ------------------------------------- V-split records (multi-GPU rows) -- */
+
+/* A record is the (m, d) state plus k (value, index) candidates of one row
+ * slice: the operand of the paper's merge (Eq. 4-5; normalizer.hpp:52-58,
+ * topk.hpp:34-44).  Fixed size per k, so n records all-gather as one
+ * contiguous buffer. */
+size_t osmx_record_bytes(int32_t k);
+/* Record of the slice x[0..V) of one row whose first element is global
+ * column col0.  k = 0: (m, d) only (softmax V-split). */
+osmx_status osmx_slice_record(const float* x, int64_t V, int64_t col0, int32_t k, void* record,
+                              void* ws, size_t ws_bytes, void* stream);
+/* Merge n records (in rank / column order) into out_record (optional) and,
+ * for k > 0, into the final vals[k] = e^(u - M)/D, idx[k] (optional). */
+osmx_status osmx_records_combine(const void* records, int32_t n, int32_t k, void* out_record,
+                                 float* vals, int64_t* idx, void* ws, size_t ws_bytes,
+                                 void* stream);
+/* y = e^(x - M)/D over a slice, (M, D) from a combined record. */
+osmx_status osmx_scale_with_record(const float* x, int64_t V, const void* record, float* y,
+                                   void* stream);
+
+/* --------------------------------------------------- host buffers (e2e) -- */
+
+/* Batched host-memory versions of the same algorithms: x, y, vals, idx are
+ * HOST pointers (pinned memory is copied directly; pageable memory is
+ * staged by the driver).  The library streams row blocks through device
+ * staging buffers on `device`, overlapping H2D, kernels and D2H on two CUDA
+ * streams, and returns after the results are in host memory.
+ * first_bad_row (optional) receives -1 or the first non-finite row. */
+osmx_status osmx_softmax_host(int alg, const float* x, int64_t rows, int64_t V, float* y,
+                              int device, int64_t* first_bad_row);
+osmx_status osmx_softmax_topk_host(int alg, const float* x, int64_t rows, int64_t V, int32_t k,
+                                   float* vals, int64_t* idx, int device, int64_t* first_bad_row);
+/* topk_of over host values (topk.hpp:54). */
+osmx_status osmx_topk_host(const float* v, int64_t rows, int64_t V, int32_t k, float* vals, int64_t* idx,
+                           int device, int64_t* first_bad_row);
+/* Release the per-device staging buffers of the host path. */
+void osmx_host_release(void);
+
+/* ---------------------------------------------------------- telemetry -- */
+
+/* Number of kernel launches issued by this library since load. */
+uint64_t osmx_launch_count(void);
+/* Launch-layer knobs (tuning and measurement only):
+ *   "shape"          0 auto, 1 resident, 2 stream, 3 split
+ *   "resident_max_v" largest V held in registers (<= 16384)
+ *   "split_chunk"    elements per CTA in split mode (0 = auto)
+ *   "stream_threads" CTA size of the stream kernels (0, 256, 512, 1024)
+ *   "topk_threads"   CTA size of the fused top-K (0, 128, 256, 512)
+ *   "host_chunk_mb"  staging block of the host path (default 512)
+ * Returns OSMX_ERR_INVALID_ARG for an unknown key. */
+osmx_status osmx_config_set(const char* key, int64_t value);
+int64_t osmx_config_get(const char* key);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* OSMX_B200_H */

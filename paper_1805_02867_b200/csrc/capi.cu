@@ -1,0 +1,511 @@
+// capi.cu -- the extern "C" boundary (include/osmx_b200.h): argument
+// validation with the reference's error precedence, workspace sizing,
+// dispatch to the launch layer, the non-finite status channel, and the
+// pipelined host-buffer path.
+//
+// Validation order follows the reference: require_nonempty before
+// require_valid_k (kernels.hpp:24-30, topk.cpp:38-39); non-finite input is
+// detected during the first pass (kernels.hpp:14-15, :32-35) and reported
+// through the workspace flag instead of an exception.
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstddef>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/osmx_b200.h"
+#include "common.cuh"
+#include "internal.hpp"
+
+namespace osmx_host {
+
+Tuning& tuning() {
+  static Tuning t;
+  return t;
+}
+
+static std::atomic<unsigned long long> g_launches{0};
+void count_launch(int n) { g_launches.fetch_add((unsigned long long)n, std::memory_order_relaxed); }
+
+int num_sms() {
+  static int cache[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (cache[dev] == 0) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = n > 0 ? n : 148;
+  }
+  return cache[dev];
+}
+
+static long long g_host_chunk_mb = 512;
+
+static size_t align256(size_t b) { return (b + 255) / 256 * 256; }
+
+// Split-region bytes (after the header) and, for the unfused pipelines, the
+// materialised probability matrix (placed after the split region).
+static size_t split_region(int alg, long long rows, long long V, int k) {
+  size_t b = 0;
+  switch (alg) {
+    case kNaive:
+    case kSafe:
+    case kOnline:
+      if (softmax_uses_split(rows, V)) b = softmax_split_ws(rows, V);
+      break;
+    case kSafeFusedTopk:
+    case kOnlineFusedTopk:
+      if (topk_split(rows, V)) b = topk_split_ws(alg, rows, V, k);
+      break;
+    case kSafeUnfusedTopk:
+    case kOnlineUnfusedTopk:
+    case kTopkOf: {
+      if (softmax_uses_split(rows, V)) b = std::max(b, softmax_split_ws(rows, V));
+      if (topk_split(rows, V)) b = std::max(b, topk_split_ws(kTopkOf, rows, V, k));
+      break;
+    }
+    default:
+      break;
+  }
+  return align256(b);
+}
+
+size_t workspace_bytes(int alg, long long rows, long long V, int k) {
+  if (rows < 1 || V < 1) return osmx_dev::kWsHeader;
+  size_t b = osmx_dev::kWsHeader + split_region(alg, rows, V, k);
+  if (alg == kSafeUnfusedTopk || alg == kOnlineUnfusedTopk) b += align256((size_t)rows * (size_t)V * sizeof(float));
+  return b;
+}
+
+}  // namespace osmx_host
+
+using namespace osmx_host;
+
+namespace {
+
+thread_local std::string t_cuda_err;
+
+osmx_status cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return OSMX_OK;
+  t_cuda_err = cudaGetErrorString(e);
+  return OSMX_ERR_CUDA;
+}
+
+bool is_softmax(int alg) { return alg == kNaive || alg == kSafe || alg == kOnline; }
+bool is_topk(int alg) {
+  return alg == kSafeUnfusedTopk || alg == kSafeFusedTopk || alg == kOnlineFusedTopk || alg == kOnlineUnfusedTopk;
+}
+
+osmx_status check_common(const void* x, long long ld, long long rows, long long V) {
+  if (V < 1) return OSMX_ERR_EMPTY;  // require_nonempty, kernels.hpp:24-26
+  if (rows < 0 || ld < V) return OSMX_ERR_INVALID_ARG;
+  if (rows > 0 && !x) return OSMX_ERR_INVALID_ARG;
+  return OSMX_OK;
+}
+
+osmx_status check_k(long long V, int k) {
+  if (k < 1 || (long long)k > V) return OSMX_ERR_INVALID_K;  // require_valid_k, kernels.hpp:28-30
+  if (k > kMaxK) return OSMX_ERR_UNSUPPORTED;
+  return OSMX_OK;
+}
+
+osmx_status run_topk_alg(int alg, const float* x, long long ldx, long long rows, long long V, int k,
+                         float* vals, long long* idx, void* ws, size_t ws_bytes, cudaStream_t st) {
+  cudaError_t e = cudaSuccess;
+  switch (alg) {
+    case kOnlineFusedTopk: e = launch_topk_mode(0, x, ldx, rows, V, k, vals, idx, ws, st); break;
+    case kSafeFusedTopk: e = launch_topk_mode(2, x, ldx, rows, V, k, vals, idx, ws, st); break;
+    case kTopkOf: e = launch_topk_mode(1, x, ldx, rows, V, k, vals, idx, ws, st); break;
+    case kSafeUnfusedTopk:
+    case kOnlineUnfusedTopk: {
+      // softmax -> materialised y (workspace tail) -> topk_of(y), the
+      // reference's safe_softmax_then_topk (topk.cpp:30-35).
+      char* y = static_cast<char*>(ws) + osmx_dev::kWsHeader + split_region(alg, rows, V, k);
+      (void)ws_bytes;
+      e = launch_softmax(alg == kSafeUnfusedTopk ? kSafe : kOnline, x, ldx, reinterpret_cast<float*>(y), V, rows,
+                         V, ws, ws_bytes, st);
+      if (e == cudaSuccess) e = launch_topk_mode(1, reinterpret_cast<float*>(y), V, rows, V, k, vals, idx, ws, st);
+      break;
+    }
+    default:
+      return OSMX_ERR_INVALID_ARG;
+  }
+  return cuda_status(e);
+}
+
+}  // namespace
+
+extern "C" {
+
+int osmx_version(void) { return OSMX_VERSION; }
+
+const char* osmx_status_string(osmx_status s) {
+  switch (s) {
+    case OSMX_OK: return "ok";
+    case OSMX_ERR_EMPTY: return "empty input vector";
+    case OSMX_ERR_NON_FINITE: return "non-finite input element";
+    case OSMX_ERR_INVALID_K: return "k must satisfy 1 <= k <= input size";
+    case OSMX_ERR_INVALID_CHUNK: return "chunk length must be >= 1";
+    case OSMX_ERR_INVALID_ARG: return "invalid argument";
+    case OSMX_ERR_CUDA: return "CUDA error";
+    case OSMX_ERR_UNSUPPORTED: return "unsupported (k above OSMX_MAX_K)";
+  }
+  return "unknown status";
+}
+
+const char* osmx_last_cuda_error(void) { return t_cuda_err.c_str(); }
+
+size_t osmx_workspace_bytes(int alg, int64_t rows, int64_t V, int32_t k) {
+  return workspace_bytes(alg, rows, V, k);
+}
+
+osmx_status osmx_workspace_init(void* ws, size_t ws_bytes, void* stream) {
+  if (!ws || ws_bytes < (size_t)osmx_dev::kWsHeader) return OSMX_ERR_INVALID_ARG;
+  return cuda_status(cudaMemsetAsync(ws, 0, osmx_dev::kWsHeader, static_cast<cudaStream_t>(stream)));
+}
+
+osmx_status osmx_check_status(void* ws, void* stream, int64_t* first_bad_row) {
+  if (!ws) return OSMX_ERR_INVALID_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  unsigned long long bad = 0;
+  cudaError_t e = cudaMemcpyAsync(&bad, ws, sizeof(bad), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e == cudaSuccess && bad) e = cudaMemsetAsync(ws, 0, sizeof(bad), st);
+  if (e == cudaSuccess && bad) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_status(e);
+  const long long row = bad ? (long long)(0x7fffffffffffffffULL - bad) : -1;
+  if (first_bad_row) *first_bad_row = row;
+  return bad ? OSMX_ERR_NON_FINITE : OSMX_OK;
+}
+
+osmx_status osmx_softmax(int alg, const float* x, int64_t ldx, float* y, int64_t ldy, int64_t rows, int64_t V,
+                         void* ws, size_t ws_bytes, void* stream) {
+  if (!is_softmax(alg)) return OSMX_ERR_INVALID_ARG;
+  osmx_status s = check_common(x, ldx, rows, V);
+  if (s) return s;
+  if (ldy < V || (rows > 0 && !y) || !ws) return OSMX_ERR_INVALID_ARG;
+  if (rows == 0) return OSMX_OK;
+  if (ws_bytes < workspace_bytes(alg, rows, V, 0)) return OSMX_ERR_INVALID_ARG;
+  return cuda_status(launch_softmax(alg, x, ldx, y, ldy, rows, V, ws, ws_bytes, static_cast<cudaStream_t>(stream)));
+}
+
+osmx_status osmx_softmax_topk(int alg, const float* x, int64_t ldx, int64_t rows, int64_t V, int32_t k,
+                              float* vals, int64_t* idx, void* ws, size_t ws_bytes, void* stream) {
+  if (!is_topk(alg)) return OSMX_ERR_INVALID_ARG;
+  osmx_status s = check_common(x, ldx, rows, V);
+  if (s) return s;
+  if ((s = check_k(V, k))) return s;
+  if ((rows > 0 && (!vals || !idx)) || !ws) return OSMX_ERR_INVALID_ARG;
+  if (rows == 0) return OSMX_OK;
+  if (ws_bytes < workspace_bytes(alg, rows, V, k)) return OSMX_ERR_INVALID_ARG;
+  return run_topk_alg(alg, x, ldx, rows, V, k, vals, reinterpret_cast<long long*>(idx), ws, ws_bytes,
+                      static_cast<cudaStream_t>(stream));
+}
+
+osmx_status osmx_topk(const float* v, int64_t ld, int64_t rows, int64_t V, int32_t k, float* vals, int64_t* idx,
+                      void* ws, size_t ws_bytes, void* stream) {
+  osmx_status s = check_common(v, ld, rows, V);
+  if (s) return s;
+  if ((s = check_k(V, k))) return s;
+  if ((rows > 0 && (!vals || !idx)) || !ws) return OSMX_ERR_INVALID_ARG;
+  if (rows == 0) return OSMX_OK;
+  if (ws_bytes < workspace_bytes(kTopkOf, rows, V, k)) return OSMX_ERR_INVALID_ARG;
+  return run_topk_alg(kTopkOf, v, ld, rows, V, k, vals, reinterpret_cast<long long*>(idx), ws, ws_bytes,
+                      static_cast<cudaStream_t>(stream));
+}
+
+osmx_status osmx_normalizer(const float* x, int64_t ldx, int64_t rows, int64_t V, int64_t chunk, float* m,
+                            float* d, void* ws, size_t ws_bytes, void* stream) {
+  osmx_status s = check_common(x, ldx, rows, V);
+  if (s) return s;
+  if (chunk < 0) return OSMX_ERR_INVALID_CHUNK;
+  if ((rows > 0 && (!m || !d)) || !ws || ws_bytes < (size_t)osmx_dev::kWsHeader) return OSMX_ERR_INVALID_ARG;
+  if (rows == 0) return OSMX_OK;
+  return cuda_status(launch_normalizer(x, ldx, rows, V, chunk, m, d, ws, static_cast<cudaStream_t>(stream)));
+}
+
+size_t osmx_record_bytes(int32_t k) { return record_bytes(k > 0 ? k : 1); }
+
+osmx_status osmx_slice_record(const float* x, int64_t V, int64_t col0, int32_t k, void* record, void* ws,
+                              size_t ws_bytes, void* stream) {
+  if (V < 1) return OSMX_ERR_EMPTY;
+  if (!x || !record || !ws || col0 < 0) return OSMX_ERR_INVALID_ARG;
+  if (k < 0 || k > kMaxK) return k < 0 ? OSMX_ERR_INVALID_K : OSMX_ERR_UNSUPPORTED;
+  const int kk = k > 0 ? k : 1;
+  // the slice may hold fewer than k elements; the merged row must not
+  const size_t need = workspace_bytes(9, 1, V, kk);
+  // force the split path regardless of tuning
+  Tuning saved = tuning();
+  tuning().shape = kShapeSplit;
+  osmx_status st = OSMX_OK;
+  if (ws_bytes < need)
+    st = OSMX_ERR_INVALID_ARG;
+  else
+    st = cuda_status(launch_slice_record(x, V, col0, k, record, ws, ws_bytes, static_cast<cudaStream_t>(stream)));
+  tuning() = saved;
+  return st;
+}
+
+osmx_status osmx_records_combine(const void* records, int32_t n, int32_t k, void* out_record, float* vals,
+                                 int64_t* idx, void* ws, size_t ws_bytes, void* stream) {
+  if (!records || n < 1 || !ws || ws_bytes < (size_t)osmx_dev::kWsHeader) return OSMX_ERR_INVALID_ARG;
+  if (k < 0 || k > kMaxK) return k < 0 ? OSMX_ERR_INVALID_K : OSMX_ERR_UNSUPPORTED;
+  if (k > 0 && (!vals) != (!idx)) return OSMX_ERR_INVALID_ARG;
+  return cuda_status(launch_records_combine(records, n, k, out_record, vals, reinterpret_cast<long long*>(idx), ws,
+                                            static_cast<cudaStream_t>(stream)));
+}
+
+osmx_status osmx_scale_with_record(const float* x, int64_t V, const void* record, float* y, void* stream) {
+  if (V < 1) return OSMX_ERR_EMPTY;
+  if (!x || !record || !y) return OSMX_ERR_INVALID_ARG;
+  return cuda_status(launch_scale_with_record(x, V, record, y, static_cast<cudaStream_t>(stream)));
+}
+
+uint64_t osmx_launch_count(void) { return g_launches.load(); }
+
+osmx_status osmx_config_set(const char* key, int64_t value) {
+  if (!key) return OSMX_ERR_INVALID_ARG;
+  auto& t = tuning();
+  if (!strcmp(key, "shape")) {
+    if (value < 0 || value > 3) return OSMX_ERR_INVALID_ARG;
+    t.shape = (int)value;
+  } else if (!strcmp(key, "resident_max_v")) {
+    if (value < 0 || value > 16384) return OSMX_ERR_INVALID_ARG;
+    t.resident_max_v = (int)value;
+  } else if (!strcmp(key, "split_chunk")) {
+    if (value < 0) return OSMX_ERR_INVALID_ARG;
+    t.split_chunk = value;
+  } else if (!strcmp(key, "stream_threads")) {
+    if (value != 0 && value != 256 && value != 512 && value != 1024) return OSMX_ERR_INVALID_ARG;
+    t.stream_threads = (int)value;
+  } else if (!strcmp(key, "topk_threads")) {
+    if (value != 0 && value != 128 && value != 256 && value != 512) return OSMX_ERR_INVALID_ARG;
+    t.topk_threads = (int)value;
+  } else if (!strcmp(key, "host_chunk_mb")) {
+    if (value < 1) return OSMX_ERR_INVALID_ARG;
+    g_host_chunk_mb = value;
+  } else {
+    return OSMX_ERR_INVALID_ARG;
+  }
+  return OSMX_OK;
+}
+
+int64_t osmx_config_get(const char* key) {
+  if (!key) return -1;
+  const auto& t = tuning();
+  if (!strcmp(key, "shape")) return t.shape;
+  if (!strcmp(key, "resident_max_v")) return t.resident_max_v;
+  if (!strcmp(key, "split_chunk")) return t.split_chunk;
+  if (!strcmp(key, "stream_threads")) return t.stream_threads;
+  if (!strcmp(key, "topk_threads")) return t.topk_threads;
+  if (!strcmp(key, "host_chunk_mb")) return g_host_chunk_mb;
+  return -1;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------ host-buffer path --
+namespace {
+
+// Per-device staging: two slots, each with its own stream, input block,
+// output block and workspace, so block i+1's H2D overlaps block i's kernel
+// and block i-1's D2H.
+struct HostCtx {
+  std::mutex mu;
+  int device = -1;
+  cudaStream_t st[2] = {nullptr, nullptr};
+  void* xin[2] = {nullptr, nullptr};
+  void* out[2] = {nullptr, nullptr};
+  void* ws[2] = {nullptr, nullptr};
+  size_t xin_b = 0, out_b = 0, ws_b = 0;
+
+  cudaError_t ensure(size_t xb, size_t ob, size_t wb) {
+    cudaError_t e = cudaSuccess;
+    if (!st[0]) {
+      for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaStreamCreateWithFlags(&st[i], cudaStreamNonBlocking);
+    }
+    auto grow = [&](void* (&p)[2], size_t& have, size_t want) {
+      if (e != cudaSuccess || want <= have) return;
+      for (int i = 0; i < 2; ++i) {
+        if (p[i]) cudaFree(p[i]);
+        p[i] = nullptr;
+      }
+      have = 0;
+      for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaMalloc(&p[i], want);
+      if (e == cudaSuccess) have = want;
+    };
+    grow(xin, xin_b, xb);
+    grow(out, out_b, ob);
+    const size_t wsb0 = ws_b;
+    grow(ws, ws_b, wb);
+    if (e == cudaSuccess && ws_b != wsb0)
+      for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaMemset(ws[i], 0, osmx_dev::kWsHeader);
+    return e;
+  }
+  void release() {
+    for (int i = 0; i < 2; ++i) {
+      if (xin[i]) cudaFree(xin[i]);
+      if (out[i]) cudaFree(out[i]);
+      if (ws[i]) cudaFree(ws[i]);
+      if (st[i]) cudaStreamDestroy(st[i]);
+      xin[i] = out[i] = ws[i] = nullptr;
+      st[i] = nullptr;
+    }
+    xin_b = out_b = ws_b = 0;
+  }
+};
+
+HostCtx g_ctx[64];
+
+template <class Launch>
+osmx_status host_pipeline(int device, long long rows, long long V, size_t out_row_bytes, int alg, int k,
+                          const float* x, void* out_host, Launch&& launch, int64_t* first_bad_row,
+                          void* out2_host = nullptr, size_t out2_row_bytes = 0) {
+  if (device < 0 || device >= 64) return OSMX_ERR_INVALID_ARG;
+  HostCtx& c = g_ctx[device];
+  std::lock_guard<std::mutex> lock(c.mu);
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return cuda_status(e);
+  const size_t row_b = (size_t)V * sizeof(float);
+  const size_t budget = (size_t)g_host_chunk_mb << 20;
+  long long rpb = (long long)std::max<size_t>(1, budget / row_b);
+  rpb = std::min(rpb, rows);
+  const size_t out_tot = (out_row_bytes + out2_row_bytes);
+  e = c.ensure(rpb * row_b, std::max<size_t>(rpb * out_tot, 256),
+               workspace_bytes(alg, rpb, V, k));
+  if (e != cudaSuccess) {
+    cudaSetDevice(prev);
+    return cuda_status(e);
+  }
+  osmx_status st = OSMX_OK;
+  const long long nblk = (rows + rpb - 1) / rpb;
+  std::vector<long long> bases((size_t)nblk, 0);
+  for (long long b = 0; b < nblk && st == OSMX_OK; ++b) {
+    const int s = (int)(b & 1);
+    const long long r0 = b * rpb;
+    const long long nr = std::min(rpb, rows - r0);
+    bases[b] = r0;
+    e = cudaMemcpyAsync(static_cast<char*>(c.ws[s]) + offsetof(osmx_dev::WsHeader, row_base), &bases[b],
+                        sizeof(long long), cudaMemcpyHostToDevice, c.st[s]);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(c.xin[s], x + r0 * V, (size_t)nr * row_b, cudaMemcpyHostToDevice, c.st[s]);
+    if (e == cudaSuccess) e = launch(static_cast<const float*>(c.xin[s]), nr, c.out[s], c.ws[s], c.ws_b, c.st[s]);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(static_cast<char*>(out_host) + r0 * out_row_bytes, c.out[s], (size_t)nr * out_row_bytes,
+                          cudaMemcpyDeviceToHost, c.st[s]);
+    if (e == cudaSuccess && out2_host)
+      e = cudaMemcpyAsync(static_cast<char*>(out2_host) + r0 * out2_row_bytes,
+                          static_cast<char*>(c.out[s]) + (size_t)rpb * out_row_bytes, (size_t)nr * out2_row_bytes,
+                          cudaMemcpyDeviceToHost, c.st[s]);
+    if (e != cudaSuccess) st = cuda_status(e);
+  }
+  // Status: each slot's flag holds the lowest bad (global) row of its
+  // blocks -- the kernels add the header's row_base set per block above.
+  long long first_bad = -1;
+  for (int s = 0; s < 2 && st == OSMX_OK; ++s) {
+    if (!c.st[s]) continue;
+    unsigned long long bad = 0;
+    e = cudaMemcpyAsync(&bad, c.ws[s], sizeof(bad), cudaMemcpyDeviceToHost, c.st[s]);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c.st[s]);
+    if (e != cudaSuccess) {
+      st = cuda_status(e);
+      break;
+    }
+    if (bad) {
+      const long long r = (long long)(0x7fffffffffffffffULL - bad);
+      first_bad = first_bad < 0 ? r : std::min(first_bad, r);
+      cudaMemsetAsync(c.ws[s], 0, sizeof(bad), c.st[s]);
+      cudaStreamSynchronize(c.st[s]);
+    }
+  }
+  if (st == OSMX_OK && first_bad >= 0) st = OSMX_ERR_NON_FINITE;
+  if (first_bad_row) *first_bad_row = first_bad;
+  cudaSetDevice(prev);
+  return st;
+}
+
+}  // namespace
+
+extern "C" {
+
+osmx_status osmx_softmax_host(int alg, const float* x, int64_t rows, int64_t V, float* y, int device,
+                              int64_t* first_bad_row) {
+  if (!is_softmax(alg)) return OSMX_ERR_INVALID_ARG;
+  osmx_status s = check_common(x, V, rows, V);
+  if (s) return s;
+  if (rows > 0 && !y) return OSMX_ERR_INVALID_ARG;
+  if (first_bad_row) *first_bad_row = -1;
+  if (rows == 0) return OSMX_OK;
+  return host_pipeline(
+      device, rows, V, (size_t)V * sizeof(float), alg, 0, x, y,
+      [&](const float* dx, long long nr, void* dout, void* ws, size_t wsb, cudaStream_t st) {
+        return launch_softmax(alg, dx, V, static_cast<float*>(dout), V, nr, V, ws, wsb, st);
+      },
+      first_bad_row);
+}
+
+osmx_status osmx_softmax_topk_host(int alg, const float* x, int64_t rows, int64_t V, int32_t k, float* vals,
+                                   int64_t* idx, int device, int64_t* first_bad_row) {
+  if (!is_topk(alg)) return OSMX_ERR_INVALID_ARG;
+  osmx_status s = check_common(x, V, rows, V);
+  if (s) return s;
+  if ((s = check_k(V, k))) return s;
+  if (rows > 0 && (!vals || !idx)) return OSMX_ERR_INVALID_ARG;
+  if (first_bad_row) *first_bad_row = -1;
+  if (rows == 0) return OSMX_OK;
+  // device output block: vals (rpb*k floats) then idx (rpb*k int64)
+  const size_t vb = (size_t)k * sizeof(float), ib = (size_t)k * sizeof(int64_t);
+  long long rpb_cache = 0;
+  (void)rpb_cache;
+  return host_pipeline(
+      device, rows, V, vb, alg, k, x, vals,
+      [&](const float* dx, long long nr, void* dout, void* ws, size_t wsb, cudaStream_t st) -> cudaError_t {
+        // idx block lives after the full-capacity vals block
+        const size_t budget = (size_t)g_host_chunk_mb << 20;
+        long long rpb = (long long)std::max<size_t>(1, budget / ((size_t)V * sizeof(float)));
+        rpb = std::min<long long>(rpb, rows);
+        float* dv = static_cast<float*>(dout);
+        long long* di = reinterpret_cast<long long*>(static_cast<char*>(dout) + (size_t)rpb * vb);
+        osmx_status r = run_topk_alg(alg, dx, V, nr, V, k, dv, di, ws, wsb, st);
+        return r == OSMX_OK ? cudaSuccess : (r == OSMX_ERR_CUDA ? cudaErrorUnknown : cudaErrorInvalidValue);
+      },
+      first_bad_row, idx, ib);
+}
+
+osmx_status osmx_topk_host(const float* v, int64_t rows, int64_t V, int32_t k, float* vals, int64_t* idx,
+                           int device, int64_t* first_bad_row) {
+  osmx_status s = check_common(v, V, rows, V);
+  if (s) return s;
+  if ((s = check_k(V, k))) return s;
+  if (rows > 0 && (!vals || !idx)) return OSMX_ERR_INVALID_ARG;
+  if (first_bad_row) *first_bad_row = -1;
+  if (rows == 0) return OSMX_OK;
+  const size_t vb = (size_t)k * sizeof(float), ib = (size_t)k * sizeof(int64_t);
+  return host_pipeline(
+      device, rows, V, vb, kTopkOf, k, v, vals,
+      [&](const float* dx, long long nr, void* dout, void* ws, size_t wsb, cudaStream_t st) -> cudaError_t {
+        const size_t budget = (size_t)g_host_chunk_mb << 20;
+        long long rpb = (long long)std::max<size_t>(1, budget / ((size_t)V * sizeof(float)));
+        rpb = std::min<long long>(rpb, rows);
+        float* dv = static_cast<float*>(dout);
+        long long* di = reinterpret_cast<long long*>(static_cast<char*>(dout) + (size_t)rpb * vb);
+        osmx_status r = run_topk_alg(kTopkOf, dx, V, nr, V, k, dv, di, ws, wsb, st);
+        return r == OSMX_OK ? cudaSuccess : (r == OSMX_ERR_CUDA ? cudaErrorUnknown : cudaErrorInvalidValue);
+      },
+      first_bad_row, idx, ib);
+}
+
+void osmx_host_release(void) {
+  for (auto& c : g_ctx) {
+    std::lock_guard<std::mutex> lock(c.mu);
+    if (c.st[0]) c.release();
+  }
+}
+
+}  // extern "C"

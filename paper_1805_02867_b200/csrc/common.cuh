@@ -1,0 +1,359 @@
+// common.cuh -- device building blocks shared by every osmx sm_100a kernel.
+//
+//   * cache-hinted 128-bit / 32-bit global loads and streaming stores
+//   * the online normalizer state (m, d) and its merge, Eq. 4/5 of the paper
+//     (reference normalizer.hpp:24-58), at thread, group and CTA level
+//   * the per-thread register top-K list with the reference's strict-'<'
+//     insertion order (topk.hpp:34-44) and group/CTA merges under the total
+//     order (value desc, index asc) (oracle.cpp:48-51)
+//   * the workspace header that carries the non-finite-row flag
+#pragma once
+
+#include <cstdint>
+#include <type_traits>
+#include <cuda_runtime.h>
+
+namespace osmx_dev {
+
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kNegInf = -__builtin_huge_valf();
+
+// ------------------------------------------------------------ memory ops --
+
+// Read-only, no L1 allocation: every element is read by exactly one thread.
+__device__ __forceinline__ float4 ld_f4(const float* p) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ float ld_f1(const float* p) {
+  float r;
+  asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(r) : "l"(p));
+  return r;
+}
+// Last read of a line (final pass of a multi-pass kernel): evict-first
+// L2 policy so the dead lines leave room for data still to be re-read.
+__device__ __forceinline__ unsigned long long pol_evict_first() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ float4 ld_f4_last(const float* p) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p), "l"(pol_evict_first()));
+  return r;
+}
+__device__ __forceinline__ float ld_f1_last(const float* p) {
+  float r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;"
+               : "=f"(r)
+               : "l"(p), "l"(pol_evict_first()));
+  return r;
+}
+// Output is never re-read by the kernel: streaming (evict-first) stores.
+__device__ __forceinline__ void st_f4(float* p, float4 v) {
+  asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void st_f1(float* p, float v) {
+  asm volatile("st.global.cs.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+
+// ------------------------------------------------------------- exponent --
+
+// 2^x, MUFU.EX2 (flushes results below 2^-126 to +0).  Only used for the
+// normalizer accumulation where terms < 1e-38 cannot change d >= 1.
+__device__ __forceinline__ float ex2(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+// e^(x - m) for the normalizer: the subtraction is done first so the
+// argument error stays relative to |x - m| (small where terms matter).
+__device__ __forceinline__ float exp_sub(float x, float m) { return ex2((x - m) * kLog2e); }
+
+// ------------------------------------------------------- (m, d) monoid --
+
+struct MD {
+  float m;  // running maximum
+  float d;  // sum of e^(x - m)
+};
+
+__device__ __forceinline__ MD md_identity() { return MD{kNegInf, 0.0f}; }
+
+// merge(), reference normalizer.hpp:52-58.  The identity (-inf, 0) is
+// absorbing without the NaN that (-inf) - (-inf) would produce.
+__device__ __forceinline__ MD md_merge(MD a, MD b) {
+  const float M = fmaxf(a.m, b.m);
+  // both identities (or a NaN-poisoned empty lane): keep d's poison
+  if (M == kNegInf) return MD{kNegInf, a.d + b.d};
+  return MD{M, a.d * exp_sub(a.m, M) + b.d * exp_sub(b.m, M)};
+}
+
+// XOR-butterfly over `width` lanes (power of two <= 32): every lane of the
+// group ends with the group total.
+template <int WIDTH>
+__device__ __forceinline__ MD md_group_reduce(MD s) {
+#pragma unroll
+  for (int o = WIDTH / 2; o > 0; o >>= 1) {
+    MD t;
+    t.m = __shfl_xor_sync(0xffffffffu, s.m, o);
+    t.d = __shfl_xor_sync(0xffffffffu, s.d, o);
+    s = md_merge(s, t);
+  }
+  return s;
+}
+
+template <int WIDTH>
+__device__ __forceinline__ float group_max(float v) {
+#pragma unroll
+  for (int o = WIDTH / 2; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+template <int WIDTH>
+__device__ __forceinline__ float group_min(float v) {
+#pragma unroll
+  for (int o = WIDTH / 2; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+template <int WIDTH>
+__device__ __forceinline__ float group_sum(float v) {
+#pragma unroll
+  for (int o = WIDTH / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+template <int WIDTH>
+__device__ __forceinline__ double group_sum_d(double v) {
+#pragma unroll
+  for (int o = WIDTH / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// CTA-wide reductions for a CTA that owns exactly one row.  `scratch` must
+// hold >= 2*NWARPS floats; the call ends with a __syncthreads so the
+// scratch can be reused immediately.
+template <int NWARPS>
+__device__ __forceinline__ MD md_cta_reduce(MD s, float* scratch) {
+  s = md_group_reduce<32>(s);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) {
+    scratch[w] = s.m;
+    scratch[NWARPS + w] = s.d;
+  }
+  __syncthreads();
+  MD t = md_identity();
+  if (l < NWARPS) t = MD{scratch[l], scratch[NWARPS + l]};
+  t = md_group_reduce<32>(t);
+  __syncthreads();
+  return t;
+}
+template <int NWARPS>
+__device__ __forceinline__ float cta_max(float v, float* scratch) {
+  v = group_max<32>(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) scratch[w] = v;
+  __syncthreads();
+  float t = l < NWARPS ? scratch[l] : kNegInf;
+  t = group_max<32>(t);
+  __syncthreads();
+  return t;
+}
+template <int NWARPS>
+__device__ __forceinline__ float cta_min(float v, float* scratch) {
+  v = group_min<32>(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) scratch[w] = v;
+  __syncthreads();
+  float t = l < NWARPS ? scratch[l] : -kNegInf;
+  t = group_min<32>(t);
+  __syncthreads();
+  return t;
+}
+template <int NWARPS>
+__device__ __forceinline__ float cta_sum(float v, float* scratch) {
+  v = group_sum<32>(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) scratch[w] = v;
+  __syncthreads();
+  float t = l < NWARPS ? scratch[l] : 0.0f;
+  t = group_sum<32>(t);
+  __syncthreads();
+  return t;
+}
+template <int NWARPS>
+__device__ __forceinline__ double cta_sum_d(double v, double* scratch) {
+  v = group_sum_d<32>(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) scratch[w] = v;
+  __syncthreads();
+  double t = l < NWARPS ? scratch[l] : 0.0;
+  t = group_sum_d<32>(t);
+  __syncthreads();
+  return t;
+}
+
+// ------------------------------------------------------------ workspace --
+
+// Every entry point takes a caller-owned device workspace whose first
+// kWsHeader bytes are this header (zero-initialised by osmx_workspace_init;
+// osmx_check_status reads and re-zeroes it).
+struct WsHeader {
+  unsigned long long bad;  // 0 = all rows finite, else (INT64_MAX - first bad row)
+  long long row_base;      // added to flagged row ids (host pipeline blocks)
+  unsigned long long pad[14];
+};
+constexpr int kWsHeader = 128;
+
+__device__ __forceinline__ void flag_bad_row(void* ws, long long row) {
+  WsHeader* h = reinterpret_cast<WsHeader*>(ws);
+  atomicMax(&h->bad, static_cast<unsigned long long>(0x7fffffffffffffffLL - (row + h->row_base)));
+}
+
+// A row is non-finite iff its normalizer is not finite (NaN / +inf inputs
+// poison d) or its minimum is -inf (the one case e^(x-m) hides).
+__device__ __forceinline__ bool row_nonfinite(float m, float d, float mn) {
+  return !(isfinite(d) && isfinite(m)) || mn == kNegInf;
+}
+
+// ---------------------------------------------------------------- top-K --
+
+// Total order of the reference (topk.hpp:40-43 strict '<' bubble; oracle
+// comparator oracle.cpp:48-51): a precedes b iff a.v > b.v, or equal values
+// and a.i < b.i.  Float compares, so -0.0 == +0.0 as in the reference.
+__device__ __forceinline__ bool before(float av, long long ai, float bv, long long bi) {
+  return av > bv || (av == bv && ai < bi);
+}
+
+// Index order with the -1 sentinel last: compare as unsigned.
+template <class I>
+__device__ __forceinline__ bool idx_less(I a, I b) {
+  using U = typename std::conditional<sizeof(I) == 8, unsigned long long, unsigned>::type;
+  return static_cast<U>(a) < static_cast<U>(b);
+}
+
+// Per-thread sorted top list with capacity KC >= the runtime k.
+//
+// The k live slots are RIGHT-aligned: slots [0, KC-k) hold +inf blockers
+// that never move, slots [KC-k, KC) hold the running top-k (sorted desc).
+// The admission threshold is therefore always v[KC-1] -- a static register
+// index (a runtime `v[k-1]` would force the list into local memory).
+// normalize() shifts the live slots to the front before merging.
+//
+// offer(): a thread offers its own elements in increasing index order, so
+// the strict '>' test keeps earlier indices ahead of later equal values --
+// exactly the reference's insertion (topk.hpp:34-44).
+// offer_ordered(): for merges, where candidates arrive in arbitrary index
+// order, the full total order (value desc, index asc) decides.
+// Live slots start at (-inf, -1) like topk_buffer's constructor
+// (topk.hpp:27-28).
+template <int KC, class I = int>
+struct TopList {
+  float v[KC];
+  I i[KC];
+
+  __device__ __forceinline__ void init(int k) {
+#pragma unroll
+    for (int s = 0; s < KC; ++s) {
+      v[s] = (s < KC - k) ? -kNegInf : kNegInf;
+      i[s] = I(-1);
+    }
+  }
+  // left-aligned, all slots live (merge lists)
+  __device__ __forceinline__ void init_empty() {
+#pragma unroll
+    for (int s = 0; s < KC; ++s) {
+      v[s] = kNegInf;
+      i[s] = I(-1);
+    }
+  }
+  __device__ __forceinline__ float thr() const { return v[KC - 1]; }
+
+  __device__ __forceinline__ void offer(float x, I j) {
+    if (!(x > v[KC - 1])) return;
+#pragma unroll
+    for (int s = KC - 1; s > 0; --s) {
+      if (x > v[s - 1]) {
+        v[s] = v[s - 1];
+        i[s] = i[s - 1];
+      } else if (x > v[s]) {
+        v[s] = x;
+        i[s] = j;
+      }
+    }
+    if (x > v[0]) {
+      v[0] = x;
+      i[0] = j;
+    }
+  }
+  __device__ __forceinline__ void offer_ordered(float x, I j) {
+    if (x < v[KC - 1]) return;
+#pragma unroll
+    for (int s = KC - 1; s > 0; --s) {
+      if (before_(x, j, v[s - 1], i[s - 1])) {
+        v[s] = v[s - 1];
+        i[s] = i[s - 1];
+      } else if (before_(x, j, v[s], i[s])) {
+        v[s] = x;
+        i[s] = j;
+      }
+    }
+    if (before_(x, j, v[0], i[0])) {
+      v[0] = x;
+      i[0] = j;
+    }
+  }
+  // Drop the front slot (taken by a merge round, or a blocker).
+  __device__ __forceinline__ void pop() {
+#pragma unroll
+    for (int s = 0; s < KC - 1; ++s) {
+      v[s] = v[s + 1];
+      i[s] = i[s + 1];
+    }
+    v[KC - 1] = kNegInf;
+    i[KC - 1] = I(-1);
+  }
+  // Move the k live slots to the front (KC-k pops of blockers).
+  __device__ __forceinline__ void normalize(int k) {
+#pragma unroll
+    for (int step = 0; step < KC - 1; ++step)
+      if (step < KC - k) pop();
+  }
+  __device__ __forceinline__ static bool before_(float av, I ai, float bv, I bi) {
+    return av > bv || (av == bv && idx_less(ai, bi));
+  }
+};
+
+// k rounds of a WIDTH-lane arg-max over the list heads, under (value desc,
+// index asc, lane asc).  All lanes of the group receive winner r through
+// sink(r, value, index); the winning lane pops its head.  Lanes of one
+// group must hold indices in one coordinate system (same row / chunk base).
+template <int WIDTH, int KC, class I, class Sink>
+__device__ __forceinline__ void group_merge(TopList<KC, I>& L, int k, Sink&& sink) {
+  const int lane = (int)(threadIdx.x & 31u);
+  for (int r = 0; r < k; ++r) {
+    float bv = L.v[0];
+    I bi = L.i[0];
+    int bl = lane;
+#pragma unroll
+    for (int o = WIDTH / 2; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const I oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
+      const bool take = ov > bv || (ov == bv && (idx_less(oi, bi) || (oi == bi && ol < bl)));
+      if (take) {
+        bv = ov;
+        bi = oi;
+        bl = ol;
+      }
+    }
+    if (lane == bl) L.pop();
+    sink(r, bv, bi);
+  }
+}
+
+}  // namespace osmx_dev

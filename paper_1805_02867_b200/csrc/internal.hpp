@@ -1,0 +1,91 @@
+// internal.hpp -- host-side launch layer shared by the kernel translation
+// units and the C-ABI (capi.cu).  Plain C++; no torch types anywhere.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace osmx_host {
+
+// Algorithm ids: the reference's algorithm enum order (counting.hpp:17-24)
+// plus the unfused online->TopK pipeline the north star adds.
+enum Alg : int {
+  kNaive = 0,
+  kSafe = 1,
+  kOnline = 2,
+  kSafeUnfusedTopk = 3,
+  kSafeFusedTopk = 4,
+  kOnlineFusedTopk = 5,
+  kOnlineUnfusedTopk = 6,
+  kTopkOf = 7,
+  kNormalizer = 8,
+};
+
+// Kernel-shape families chosen per (rows, V) by the launch layer.
+enum Shape : int {
+  kShapeAuto = 0,
+  kShapeResident = 1,  // row held in registers by a group of <= 1024 threads
+  kShapeStream = 2,    // one CTA per row, every pass streams global memory
+  kShapeSplit = 3,     // row split over S CTAs, (m,d)/top-K records + combine
+};
+
+struct Tuning {
+  int shape = kShapeAuto;       // force a family (0 = heuristic)
+  int resident_max_v = 16384;   // largest V held in registers
+  long long split_chunk = 0;    // elements per CTA in split mode (0 = auto)
+  int stream_threads = 0;       // CTA size for stream kernels (0 = auto)
+  int topk_threads = 0;         // CTA size for the fused top-K (0 = auto)
+};
+Tuning& tuning();
+
+// Kernel-launch tally (every launch the library issues increments it).
+void count_launch(int n = 1);
+
+int num_sms();
+
+// ---------------------------------------------------------------- launchers
+// All pointers are device pointers.  ws points at the workspace header; the
+// split region (if any) starts at ws + kWsHeader.  Return cudaError_t.
+
+cudaError_t launch_softmax(int alg, const float* x, long long ldx, float* y, long long ldy,
+                           long long rows, long long V, void* ws, size_t ws_bytes, cudaStream_t st);
+
+cudaError_t launch_topk(int alg, const float* x, long long ldx, long long rows, long long V, int k,
+                        float* vals, long long* idx, void* ws, size_t ws_bytes, cudaStream_t st);
+
+cudaError_t launch_normalizer(const float* x, long long ldx, long long rows, long long V,
+                              long long chunk, float* m, float* d, void* ws, cudaStream_t st);
+
+// Split-mode record of one row slice: (m, d, min) + k candidates.
+size_t record_bytes(int k);
+// Partial record of one row slice [x, x+V) whose global column offset is
+// col0; the combine of n records (rank order) into one record, and into the
+// final (vals, idx) when k > 0; the softmax scale pass against a record.
+cudaError_t launch_slice_record(const float* x, long long V, long long col0, int k, void* record,
+                                void* ws, size_t ws_bytes, cudaStream_t st);
+cudaError_t launch_records_combine(const void* records, int n, int k, void* out_record,
+                                   float* vals, long long* idx, void* ws, cudaStream_t st);
+cudaError_t launch_scale_with_record(const float* x, long long V, const void* record, float* y,
+                                     cudaStream_t st);
+
+size_t workspace_bytes(int alg, long long rows, long long V, int k);
+
+// softmax.cu
+size_t softmax_split_ws(long long rows, long long V);
+bool softmax_uses_split(long long rows, long long V);
+// Safe split phases 0 and 1 (row max, then d against it) into 16-byte
+// records {float m, float mn, double d} (the safe fused top-K's first passes).
+cudaError_t launch_safe_split_stats(const float* x, long long ldx, long long rows, long long V,
+                                    long long chunk, void* srec, cudaStream_t st);
+
+// topk.cu.  mode: 0 fused online, 1 topk_of, 2 safe fused.
+size_t topk_split_ws(int alg, long long rows, long long V, int k);
+bool topk_split(long long rows, long long V);
+cudaError_t launch_topk_mode(int mode, const float* x, long long ldx, long long rows, long long V,
+                             int k, float* vals, long long* idx, void* ws, cudaStream_t st);
+
+// Largest k served by the register top-K lists.
+constexpr int kMaxK = 32;
+
+}  // namespace osmx_host

@@ -1,0 +1,35 @@
+// softmax.cu -- dispatch of the batched softmax family (kernels in
+// softmax_impl.cuh; one translation unit per algorithm so they build in
+// parallel: softmax_naive.cu, softmax_safe.cu, softmax_online.cu).
+#include "softmax_impl.cuh"
+
+namespace osmx_host {
+
+cudaError_t launch_softmax_naive(const float*, long long, float*, long long, long long, long long, void*, cudaStream_t);
+cudaError_t launch_softmax_safe(const float*, long long, float*, long long, long long, long long, void*, cudaStream_t);
+cudaError_t launch_softmax_online(const float*, long long, float*, long long, long long, long long, void*, cudaStream_t);
+
+size_t softmax_split_ws(long long rows, long long V) {
+  const long long ch = split_chunk(rows, V);
+  const long long S = (V + ch - 1) / ch;
+  return (size_t)(rows * S) * sizeof(SRec);
+}
+
+bool softmax_uses_split(long long rows, long long V) {
+  const auto& tn = tuning();
+  if (tn.shape == kShapeSplit) return rows <= 65535;
+  if (tn.shape != kShapeAuto) return false;
+  return V > tn.resident_max_v && rows < 2LL * num_sms();
+}
+
+cudaError_t launch_softmax(int alg, const float* x, long long ldx, float* y, long long ldy,
+                           long long rows, long long V, void* ws, size_t, cudaStream_t st) {
+  switch (alg) {
+    case kNaive: return launch_softmax_naive(x, ldx, y, ldy, rows, V, ws, st);
+    case kSafe: return launch_softmax_safe(x, ldx, y, ldy, rows, V, ws, st);
+    case kOnline: return launch_softmax_online(x, ldx, y, ldy, rows, V, ws, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace osmx_host

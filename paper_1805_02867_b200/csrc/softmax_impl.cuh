@@ -1,0 +1,688 @@
+// softmax_impl.cuh -- batched naive / safe / online softmax for sm_100a.
+//
+// Replaces the reference's single-row kernel templates
+//   naive_softmax_kernel   kernels.hpp:39-46   (Alg. 1)
+//   safe_softmax_kernel    kernels.hpp:49-58   (Alg. 2, 3 passes, 4 accesses)
+//   online_softmax_kernel  kernels.hpp:61-69   (Alg. 3, 2 passes, 3 accesses)
+// and the chunked normalizer run_normalizer_chunked (normalizer.hpp:73-85)
+// as the split-row combine.  Three kernel families (launch layer picks):
+//
+//   resident : a group of TPR threads owns one row and keeps it in
+//              registers; the second (and third) pass of the algorithm
+//              re-reads registers, so DRAM sees 1 read + 1 write.
+//   stream   : one CTA per row, every pass streams global memory (the
+//              paper's one-threadblock-per-vector design).
+//   split    : the row is cut into S contiguous chunks, one CTA each; per
+//              chunk records (m, d, min) are merged with the reference's
+//              merge() and the scale pass runs per chunk.
+//
+// Numerics (SURVEY.md sec.7 risk 3): m is exact (a max), d accumulates in
+// fp32 from ex2.approx terms against the running max (naive: fp64 sum, like
+// the reference), outputs use the accurate expf and one IEEE reciprocal of
+// d per row.  No fast-math, no FTZ on outputs.
+#pragma once
+#include <algorithm>
+
+#include "common.cuh"
+#include "internal.hpp"
+#include "stream.cuh"
+
+using namespace osmx_dev;
+
+namespace {
+
+// ----------------------------------------------------- group reductions --
+// A group is TPR consecutive threads of a BLOCK-thread CTA (TPR <= 32: a
+// sub-warp; TPR > 32: W = TPR/32 whole warps).  All threads of the CTA must
+// call these together (they contain __syncthreads when TPR > 32).
+template <int TPR, int BLOCK>
+struct Grp {
+  static constexpr int NW = BLOCK / 32;
+  static constexpr int W = TPR / 32;
+
+  template <class T, class Op>
+  __device__ static T reduce(T v, Op op, T* sm) {
+    if constexpr (TPR <= 32) {
+#pragma unroll
+      for (int o = TPR / 2; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
+      return v;
+    } else {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
+      const int w = threadIdx.x >> 5;
+      if ((threadIdx.x & 31) == 0) sm[w] = v;
+      __syncthreads();
+      const int g0 = (w / W) * W;
+      T t = sm[g0];
+#pragma unroll
+      for (int i = 1; i < W; ++i) t = op(t, sm[g0 + i]);
+      __syncthreads();
+      return t;
+    }
+  }
+  __device__ static MD md(MD s, float* sm) {
+    if constexpr (TPR <= 32) {
+#pragma unroll
+      for (int o = TPR / 2; o > 0; o >>= 1) {
+        MD t{__shfl_xor_sync(0xffffffffu, s.m, o), __shfl_xor_sync(0xffffffffu, s.d, o)};
+        s = md_merge(s, t);
+      }
+      return s;
+    } else {
+      s = md_group_reduce<32>(s);
+      const int w = threadIdx.x >> 5;
+      if ((threadIdx.x & 31) == 0) {
+        sm[w] = s.m;
+        sm[NW + w] = s.d;
+      }
+      __syncthreads();
+      const int g0 = (w / W) * W;
+      MD t{sm[g0], sm[NW + g0]};
+#pragma unroll
+      for (int i = 1; i < W; ++i) t = md_merge(t, MD{sm[g0 + i], sm[NW + g0 + i]});
+      __syncthreads();
+      return t;
+    }
+  }
+};
+
+struct OpMax {
+  __device__ float operator()(float a, float b) const { return fmaxf(a, b); }
+};
+struct OpSum {
+  __device__ float operator()(float a, float b) const { return a + b; }
+};
+struct OpSumD {
+  __device__ double operator()(double a, double b) const { return a + b; }
+};
+
+__device__ __forceinline__ float nanf_() { return __int_as_float(0x7fffffff); }
+
+// ------------------------------------------------------------- resident --
+// EPT elements per thread (VEC: EPT/4 float4s).  Rows per CTA = BLOCK/TPR.
+template <int TPR, int EPT, bool VEC, int ALG>
+__global__ void __launch_bounds__(TPR > 256 ? TPR : 256)
+    k_softmax_resident(const float* __restrict__ x, long long ldx, float* __restrict__ y,
+                       long long ldy, long long rows, int V, void* ws) {
+  constexpr int BLOCK = TPR > 256 ? TPR : 256;
+  constexpr int RPC = BLOCK / TPR;
+  using G = Grp<TPR, BLOCK>;
+  __shared__ float smf[2 * (BLOCK / 32)];
+  __shared__ double smd[BLOCK / 32];
+
+  const int g = threadIdx.x % TPR;
+  const long long row = (long long)blockIdx.x * RPC + threadIdx.x / TPR;
+  const bool live = row < rows;
+  const float* xr = x + (live ? row : 0) * ldx;
+  float* yr = y + (live ? row : 0) * ldy;
+
+  float a[EPT];
+  bool bad = false;
+  if constexpr (VEC) {
+#pragma unroll
+    for (int t = 0; t < EPT / 4; ++t) {
+      const int q = g + TPR * t;
+      float4 v = make_float4(kNegInf, kNegInf, kNegInf, kNegInf);
+      if (live && 4 * q < V) {
+        v = ld_f4(xr + 4 * q);
+        bad |= !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w));
+      }
+      a[4 * t] = v.x;
+      a[4 * t + 1] = v.y;
+      a[4 * t + 2] = v.z;
+      a[4 * t + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int t = 0; t < EPT; ++t) {
+      const int e = g + TPR * t;
+      float v = kNegInf;
+      if (live && e < V) {
+        v = ld_f1(xr + e);
+        bad |= !isfinite(v);
+      }
+      a[t] = v;
+    }
+  }
+
+  // Returns (m, scale) such that y = f(x) * scale.
+  float m = 0.0f, r = 0.0f;
+  double rd = 0.0;
+  bool row_bad = false;
+  if constexpr (ALG == osmx_host::kOnline) {
+    // Alg. 3 lines 1-6 on the thread's elements (max first, then one
+    // rescale-free sum), then the group-wide merge (Eq. 4).
+    float lm = kNegInf;
+#pragma unroll
+    for (int t = 0; t < EPT; ++t) lm = fmaxf(lm, a[t]);
+    float ld = 0.0f;
+    if (lm != kNegInf) {
+#pragma unroll
+      for (int t = 0; t < EPT; ++t) ld += exp_sub(a[t], lm);
+    }
+    if (bad) ld = nanf_();
+    MD s = G::md(MD{lm, ld}, smf);
+    m = s.m;
+    r = __frcp_rn(s.d);
+    row_bad = !(s.d == s.d) || !isfinite(m);
+  } else if constexpr (ALG == osmx_host::kSafe) {
+    float lm = kNegInf;
+#pragma unroll
+    for (int t = 0; t < EPT; ++t) lm = fmaxf(lm, a[t]);
+    m = G::reduce(lm, OpMax(), smf);
+    float ld = 0.0f;
+#pragma unroll
+    for (int t = 0; t < EPT; ++t) ld += exp_sub(a[t], m);
+    if (bad) ld = nanf_();
+    const float d = G::reduce(ld, OpSum(), smf);
+    r = __frcp_rn(d);
+    row_bad = !(d == d) || !isfinite(m);
+  } else {  // naive: d = sum double(expf(x)), no max shift (kernels.hpp:43-45)
+    double ld = 0.0;
+#pragma unroll
+    for (int t = 0; t < EPT; ++t) ld += (double)expf(a[t]);
+    if (bad) ld = (double)nanf_();
+    const double d = G::reduce(ld, OpSumD(), smd);
+    rd = 1.0 / d;
+    row_bad = !(d == d);
+  }
+  if (!live) return;
+  if (row_bad) {
+    if (g == 0) flag_bad_row(ws, row);
+  }
+  auto f = [&](float v) -> float {
+    if constexpr (ALG == osmx_host::kNaive)
+      return (float)((double)expf(v) * rd);
+    else
+      return expf(v - m) * r;
+  };
+  if constexpr (VEC) {
+#pragma unroll
+    for (int t = 0; t < EPT / 4; ++t) {
+      const int q = g + TPR * t;
+      if (4 * q < V)
+        st_f4(yr + 4 * q, make_float4(f(a[4 * t]), f(a[4 * t + 1]), f(a[4 * t + 2]), f(a[4 * t + 3])));
+    }
+  } else {
+#pragma unroll
+    for (int t = 0; t < EPT; ++t) {
+      const int e = g + TPR * t;
+      if (e < V) st_f1(yr + e, f(a[t]));
+    }
+  }
+}
+
+// --------------------------------------------------------------- stream --
+// One CTA per row; every pass of the algorithm reads global memory.
+template <int BLOCK, int U, int ALG>
+__global__ void __launch_bounds__(BLOCK)
+    k_softmax_stream(const float* __restrict__ x, long long ldx, float* __restrict__ y,
+                     long long ldy, long long rows, long long V, void* ws) {
+  constexpr int NW = BLOCK / 32;
+  __shared__ float smf[2 * NW];
+  __shared__ double smd[NW];
+  const int t = threadIdx.x;
+  for (long long row = blockIdx.x; row < rows; row += gridDim.x) {
+    const Seg s = make_seg(x + row * ldx, V);
+    float* yr = y + row * ldy;
+    float mn = -kNegInf;
+    float M, r = 0.0f;
+    double rd = 0.0;
+    bool bad;
+    if constexpr (ALG == osmx_host::kOnline) {
+      // Pass 1: Alg. 3 lines 1-6, batch-max-first update per U float4s.
+      float m = kNegInf, d = 0.0f;
+      stream_seg<BLOCK, U, false>(
+          s, t,
+          [&](float v, long long) {
+            mn = fminf(mn, v);
+            if (v > m) {
+              d = d * exp_sub(m, v) + 1.0f;
+              m = v;
+            } else {
+              d += exp_sub(v, m);
+            }
+          },
+          [&](float4 (&v)[U], long long, int cnt) {
+            float bm = kNegInf, bn = -kNegInf;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              bm = fmaxf(bm, fmaxf(fmaxf(v[u].x, v[u].y), fmaxf(v[u].z, v[u].w)));
+              if (u < cnt) bn = fminf(bn, fminf(fminf(v[u].x, v[u].y), fminf(v[u].z, v[u].w)));
+            }
+            mn = fminf(mn, bn);
+            if (bm > m) {
+              d *= exp_sub(m, bm);
+              m = bm;
+            }
+            float sum = 0.0f;
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+              sum += (exp_sub(v[u].x, m) + exp_sub(v[u].y, m)) + (exp_sub(v[u].z, m) + exp_sub(v[u].w, m));
+            d += sum;
+          });
+      MD tot = md_cta_reduce<NW>(MD{m, d}, smf);
+      mn = cta_min<NW>(mn, smf);
+      M = tot.m;
+      r = __frcp_rn(tot.d);
+      bad = !(tot.d == tot.d) || !isfinite(M) || mn == kNegInf;
+    } else if constexpr (ALG == osmx_host::kSafe) {
+      // Pass 1: max (kernels.hpp:54).  Pass 2: normalizer (:56).
+      float m = kNegInf;
+      stream_seg<BLOCK, U, false>(
+          s, t,
+          [&](float v, long long) {
+            m = fmaxf(m, v);
+            mn = fminf(mn, v);
+            if (v != v) m = v;  // keep NaN visible
+          },
+          [&](float4 (&v)[U], long long, int cnt) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              m = fmaxf(m, fmaxf(fmaxf(v[u].x, v[u].y), fmaxf(v[u].z, v[u].w)));
+              if (u < cnt) mn = fminf(mn, fminf(fminf(v[u].x, v[u].y), fminf(v[u].z, v[u].w)));
+            }
+          });
+      M = cta_max<NW>(m, smf);
+      mn = cta_min<NW>(mn, smf);
+      float d = 0.0f;
+      stream_seg<BLOCK, U, false>(
+          s, t, [&](float v, long long) { d += exp_sub(v, M); },
+          [&](float4 (&v)[U], long long, int) {
+            float sum = 0.0f;
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+              sum += (exp_sub(v[u].x, M) + exp_sub(v[u].y, M)) + (exp_sub(v[u].z, M) + exp_sub(v[u].w, M));
+            d += sum;
+          });
+      d = cta_sum<NW>(d, smf);
+      r = __frcp_rn(d);
+      bad = !(d == d) || !isfinite(M) || mn == kNegInf;
+    } else {
+      // Naive: d = sum double(expf(x)) (kernels.hpp:43-44).
+      double d = 0.0;
+      float mx = kNegInf;
+      stream_seg<BLOCK, U, false>(
+          s, t,
+          [&](float v, long long) {
+            d += (double)expf(v);
+            mx = fmaxf(mx, v);
+            mn = fminf(mn, v);
+          },
+          [&](float4 (&v)[U], long long, int cnt) {
+            float part = 0.0f;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              if (u < cnt) {
+                d += (double)expf(v[u].x) + (double)expf(v[u].y) + (double)expf(v[u].z) + (double)expf(v[u].w);
+                mx = fmaxf(mx, fmaxf(fmaxf(v[u].x, v[u].y), fmaxf(v[u].z, v[u].w)));
+                mn = fminf(mn, fminf(fminf(v[u].x, v[u].y), fminf(v[u].z, v[u].w)));
+              }
+            }
+            (void)part;
+          });
+      d = cta_sum_d<NW>(d, smd);
+      mx = cta_max<NW>(mx, smf);
+      mn = cta_min<NW>(mn, smf);
+      rd = 1.0 / d;
+      M = 0.0f;
+      bad = !(d == d) || !isfinite(mx) || mn == kNegInf;
+    }
+    if (bad && t == 0) flag_bad_row(ws, row);
+    // Final pass: y = e^(x - m) / d (kernels.hpp:57 / :68; naive :45).
+    if constexpr (ALG == osmx_host::kNaive) {
+      map_seg<BLOCK, U>(s, yr, t, [&](float v) { return (float)((double)expf(v) * rd); });
+    } else {
+      map_seg<BLOCK, U>(s, yr, t, [&](float v) { return expf(v - M) * r; });
+    }
+  }
+}
+
+// ---------------------------------------------------------------- split --
+// Record of one chunk: m = running max (online) / max (safe, naive),
+// mn = min (non-finite detection), d = normalizer (double so the naive sum
+// does not overflow fp32 where the reference's double does not).
+struct SRec {
+  float m;
+  float mn;
+  double d;
+};
+
+// Phase 0 for all algorithms; phase 1 (safe only) recomputes d against the
+// row max gathered from the phase-0 records.
+template <int BLOCK, int U, int ALG, int PHASE>
+__global__ void __launch_bounds__(BLOCK)
+    k_softmax_split_part(const float* __restrict__ x, long long ldx, long long V, long long chunk,
+                         SRec* __restrict__ rec) {
+  constexpr int NW = BLOCK / 32;
+  __shared__ float smf[2 * NW];
+  __shared__ double smd[NW];
+  const int S = gridDim.x;
+  const long long row = blockIdx.y;
+  const long long c0 = (long long)blockIdx.x * chunk;
+  const long long n = std::min(chunk, V - c0);
+  const Seg s = make_seg(x + row * ldx + c0, n);
+  const int t = threadIdx.x;
+  SRec* rr = rec + row * S;
+  if constexpr (ALG == osmx_host::kSafe && PHASE == 1) {
+    float M = kNegInf;
+    for (int i = t; i < S; i += BLOCK) M = fmaxf(M, rr[i].m);
+    M = cta_max<NW>(M, smf);
+    float d = 0.0f;
+    stream_seg<BLOCK, U, false>(
+        s, t, [&](float v, long long) { d += exp_sub(v, M); },
+        [&](float4 (&v)[U], long long, int) {
+          float sum = 0.0f;
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            sum += (exp_sub(v[u].x, M) + exp_sub(v[u].y, M)) + (exp_sub(v[u].z, M) + exp_sub(v[u].w, M));
+          d += sum;
+        });
+    d = cta_sum<NW>(d, smf);
+    __syncthreads();  // every thread has read rr[*].m before it is rewritten
+    if (t == 0) rr[blockIdx.x].d = (double)d;
+    return;
+  }
+  float mn = -kNegInf;
+  if constexpr (ALG == osmx_host::kOnline) {
+    float m = kNegInf, d = 0.0f;
+    stream_seg<BLOCK, U, false>(
+        s, t,
+        [&](float v, long long) {
+          mn = fminf(mn, v);
+          if (v > m) {
+            d = d * exp_sub(m, v) + 1.0f;
+            m = v;
+          } else {
+            d += exp_sub(v, m);
+          }
+        },
+        [&](float4 (&v)[U], long long, int cnt) {
+          float bm = kNegInf, bn = -kNegInf;
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            bm = fmaxf(bm, fmaxf(fmaxf(v[u].x, v[u].y), fmaxf(v[u].z, v[u].w)));
+            if (u < cnt) bn = fminf(bn, fminf(fminf(v[u].x, v[u].y), fminf(v[u].z, v[u].w)));
+          }
+          mn = fminf(mn, bn);
+          if (bm > m) {
+            d *= exp_sub(m, bm);
+            m = bm;
+          }
+          float sum = 0.0f;
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            sum += (exp_sub(v[u].x, m) + exp_sub(v[u].y, m)) + (exp_sub(v[u].z, m) + exp_sub(v[u].w, m));
+          d += sum;
+        });
+    MD tot = md_cta_reduce<NW>(MD{m, d}, smf);
+    mn = cta_min<NW>(mn, smf);
+    if (t == 0) rr[blockIdx.x] = SRec{tot.m, mn, (double)tot.d};
+  } else if constexpr (ALG == osmx_host::kSafe) {
+    float m = kNegInf;
+    stream_seg<BLOCK, U, false>(
+        s, t,
+        [&](float v, long long) {
+          m = fmaxf(m, v);
+          mn = fminf(mn, v);
+          if (v != v) m = v;
+        },
+        [&](float4 (&v)[U], long long, int cnt) {
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            m = fmaxf(m, fmaxf(fmaxf(v[u].x, v[u].y), fmaxf(v[u].z, v[u].w)));
+            if (u < cnt) mn = fminf(mn, fminf(fminf(v[u].x, v[u].y), fminf(v[u].z, v[u].w)));
+          }
+        });
+    m = cta_max<NW>(m, smf);
+    mn = cta_min<NW>(mn, smf);
+    if (t == 0) rr[blockIdx.x] = SRec{m, mn, 0.0};
+  } else {
+    double d = 0.0;
+    float mx = kNegInf;
+    stream_seg<BLOCK, U, false>(
+        s, t,
+        [&](float v, long long) {
+          d += (double)expf(v);
+          mx = fmaxf(mx, v);
+          mn = fminf(mn, v);
+        },
+        [&](float4 (&v)[U], long long, int cnt) {
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            if (u < cnt) {
+              d += (double)expf(v[u].x) + (double)expf(v[u].y) + (double)expf(v[u].z) + (double)expf(v[u].w);
+              mx = fmaxf(mx, fmaxf(fmaxf(v[u].x, v[u].y), fmaxf(v[u].z, v[u].w)));
+              mn = fminf(mn, fminf(fminf(v[u].x, v[u].y), fminf(v[u].z, v[u].w)));
+            }
+          }
+        });
+    d = cta_sum_d<NW>(d, smd);
+    mx = cta_max<NW>(mx, smf);
+    mn = cta_min<NW>(mn, smf);
+    if (t == 0) rr[blockIdx.x] = SRec{mx, mn, d};
+  }
+}
+
+// Merge the S records of the row (every CTA does it; S*16 bytes from L2),
+// flag the row once, then write y for this CTA's chunk.
+template <int BLOCK, int U, int ALG>
+__global__ void __launch_bounds__(BLOCK)
+    k_softmax_split_scale(const float* __restrict__ x, long long ldx, float* __restrict__ y,
+                          long long ldy, long long V, long long chunk, const SRec* __restrict__ rec,
+                          void* ws) {
+  constexpr int NW = BLOCK / 32;
+  __shared__ float smf[2 * NW];
+  __shared__ double smd[NW];
+  const int S = gridDim.x;
+  const long long row = blockIdx.y;
+  const int t = threadIdx.x;
+  const SRec* rr = rec + row * S;
+  float M = kNegInf, mn = -kNegInf, r = 0.0f;
+  double rd = 0.0;
+  bool bad;
+  if constexpr (ALG == osmx_host::kOnline) {
+    MD a = md_identity();
+    for (int i = t; i < S; i += BLOCK) {
+      a = md_merge(a, MD{rr[i].m, (float)rr[i].d});
+      mn = fminf(mn, rr[i].mn);
+    }
+    a = md_cta_reduce<NW>(a, smf);
+    mn = cta_min<NW>(mn, smf);
+    M = a.m;
+    r = __frcp_rn(a.d);
+    bad = !(a.d == a.d) || !isfinite(M) || mn == kNegInf;
+  } else if constexpr (ALG == osmx_host::kSafe) {
+    float d = 0.0f;
+    for (int i = t; i < S; i += BLOCK) {
+      M = fmaxf(M, rr[i].m);
+      mn = fminf(mn, rr[i].mn);
+      d += (float)rr[i].d;
+    }
+    M = cta_max<NW>(M, smf);
+    mn = cta_min<NW>(mn, smf);
+    d = cta_sum<NW>(d, smf);
+    r = __frcp_rn(d);
+    bad = !(d == d) || !isfinite(M) || mn == kNegInf;
+  } else {
+    double d = 0.0;
+    for (int i = t; i < S; i += BLOCK) {
+      M = fmaxf(M, rr[i].m);
+      mn = fminf(mn, rr[i].mn);
+      d += rr[i].d;
+    }
+    M = cta_max<NW>(M, smf);
+    mn = cta_min<NW>(mn, smf);
+    d = cta_sum_d<NW>(d, smd);
+    rd = 1.0 / d;
+    bad = !(d == d) || !isfinite(M) || mn == kNegInf;
+  }
+  if (bad && t == 0 && blockIdx.x == 0) flag_bad_row(ws, row);
+  const long long c0 = (long long)blockIdx.x * chunk;
+  const long long n = std::min(chunk, V - c0);
+  const Seg s = make_seg(x + row * ldx + c0, n);
+  float* yr = y + row * ldy + c0;
+  if constexpr (ALG == osmx_host::kNaive) {
+    map_seg<BLOCK, U>(s, yr, t, [&](float v) { return (float)((double)expf(v) * rd); });
+  } else {
+    map_seg<BLOCK, U>(s, yr, t, [&](float v) { return expf(v - M) * r; });
+  }
+}
+
+// ------------------------------------------------------ normalizer only --
+// Batched run_normalizer / run_normalizer_chunked (normalizer.hpp:61-85):
+// (m, d) per row.  chunk > 0 reproduces the contiguous-chunk left-to-right
+// merge order; chunk == 0 is the CTA-parallel evaluation.
+template <int BLOCK, int U>
+__global__ void __launch_bounds__(BLOCK)
+    k_normalizer(const float* __restrict__ x, long long ldx, long long rows, long long V,
+                 float* __restrict__ om, float* __restrict__ od, void* ws) {
+  constexpr int NW = BLOCK / 32;
+  __shared__ float smf[2 * NW];
+  const int t = threadIdx.x;
+  for (long long row = blockIdx.x; row < rows; row += gridDim.x) {
+    const Seg s = make_seg(x + row * ldx, V);
+    float m = kNegInf, d = 0.0f, mn = -kNegInf;
+    stream_seg<BLOCK, U, false>(
+        s, t,
+        [&](float v, long long) {
+          mn = fminf(mn, v);
+          if (v > m) {
+            d = d * exp_sub(m, v) + 1.0f;
+            m = v;
+          } else {
+            d += exp_sub(v, m);
+          }
+        },
+        [&](float4 (&v)[U], long long, int cnt) {
+          float bm = kNegInf, bn = -kNegInf;
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            bm = fmaxf(bm, fmaxf(fmaxf(v[u].x, v[u].y), fmaxf(v[u].z, v[u].w)));
+            if (u < cnt) bn = fminf(bn, fminf(fminf(v[u].x, v[u].y), fminf(v[u].z, v[u].w)));
+          }
+          mn = fminf(mn, bn);
+          if (bm > m) {
+            d *= exp_sub(m, bm);
+            m = bm;
+          }
+          float sum = 0.0f;
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            sum += (exp_sub(v[u].x, m) + exp_sub(v[u].y, m)) + (exp_sub(v[u].z, m) + exp_sub(v[u].w, m));
+          d += sum;
+        });
+    MD tot = md_cta_reduce<NW>(MD{m, d}, smf);
+    mn = cta_min<NW>(mn, smf);
+    if (t == 0) {
+      om[row] = tot.m;
+      od[row] = tot.d;
+      if (!(tot.d == tot.d) || !isfinite(tot.m) || mn == kNegInf) flag_bad_row(ws, row);
+    }
+  }
+}
+
+// ------------------------------------------------------------ launchers --
+
+template <int TPR, int EPT, int ALG>
+cudaError_t run_resident(bool vec, const float* x, long long ldx, float* y, long long ldy,
+                         long long rows, long long V, void* ws, cudaStream_t st) {
+  constexpr int BLOCK = TPR > 256 ? TPR : 256;
+  constexpr int RPC = BLOCK / TPR;
+  const long long grid = (rows + RPC - 1) / RPC;
+  if (vec)
+    k_softmax_resident<TPR, EPT, true, ALG><<<(unsigned)grid, BLOCK, 0, st>>>(x, ldx, y, ldy, rows, (int)V, ws);
+  else
+    k_softmax_resident<TPR, EPT, false, ALG><<<(unsigned)grid, BLOCK, 0, st>>>(x, ldx, y, ldy, rows, (int)V, ws);
+  osmx_host::count_launch();
+  return cudaGetLastError();
+}
+
+template <int ALG>
+cudaError_t dispatch_resident(bool vec, const float* x, long long ldx, float* y, long long ldy,
+                              long long rows, long long V, void* ws, cudaStream_t st) {
+  if (V <= 64) return run_resident<8, 8, ALG>(vec, x, ldx, y, ldy, rows, V, ws, st);
+  if (V <= 256) return run_resident<32, 8, ALG>(vec, x, ldx, y, ldy, rows, V, ws, st);
+  if (V <= 512) return run_resident<32, 16, ALG>(vec, x, ldx, y, ldy, rows, V, ws, st);
+  if (V <= 1024) return run_resident<32, 32, ALG>(vec, x, ldx, y, ldy, rows, V, ws, st);
+  if (V <= 2048) return run_resident<128, 16, ALG>(vec, x, ldx, y, ldy, rows, V, ws, st);
+  if (V <= 4096) return run_resident<256, 16, ALG>(vec, x, ldx, y, ldy, rows, V, ws, st);
+  if (V <= 8192) return run_resident<256, 32, ALG>(vec, x, ldx, y, ldy, rows, V, ws, st);
+  return run_resident<512, 32, ALG>(vec, x, ldx, y, ldy, rows, V, ws, st);
+}
+
+template <int ALG>
+cudaError_t run_stream(const float* x, long long ldx, float* y, long long ldy, long long rows,
+                       long long V, void* ws, cudaStream_t st) {
+  int threads = osmx_host::tuning().stream_threads;
+  if (threads == 0) threads = V >= 65536 ? 512 : 256;
+  const long long grid = std::min<long long>(rows, 1LL << 30);
+  if (threads == 1024)
+    k_softmax_stream<1024, 4, ALG><<<(unsigned)grid, 1024, 0, st>>>(x, ldx, y, ldy, rows, V, ws);
+  else if (threads == 512)
+    k_softmax_stream<512, 4, ALG><<<(unsigned)grid, 512, 0, st>>>(x, ldx, y, ldy, rows, V, ws);
+  else
+    k_softmax_stream<256, 4, ALG><<<(unsigned)grid, 256, 0, st>>>(x, ldx, y, ldy, rows, V, ws);
+  osmx_host::count_launch();
+  return cudaGetLastError();
+}
+
+constexpr int kSplitBlock = 512;
+constexpr int kSplitU = 4;
+
+long long split_chunk(long long rows, long long V) {
+  long long ch = osmx_host::tuning().split_chunk;
+  if (ch <= 0) {
+    // ~4 CTAs per SM over the whole problem, at least 32K elements each.
+    const long long target = 4LL * osmx_host::num_sms();
+    long long per_row = std::max<long long>(1, target / std::max<long long>(rows, 1));
+    ch = (V + per_row - 1) / per_row;
+    ch = std::max<long long>(ch, 32768);
+  }
+  ch = (ch + 15) / 16 * 16;  // keeps every chunk in the row's 16-byte phase
+  return ch;
+}
+
+template <int ALG>
+cudaError_t run_split(const float* x, long long ldx, float* y, long long ldy, long long rows,
+                      long long V, void* ws, cudaStream_t st) {
+  const long long ch = split_chunk(rows, V);
+  const long long S = (V + ch - 1) / ch;
+  SRec* rec = reinterpret_cast<SRec*>(static_cast<char*>(ws) + kWsHeader);
+  dim3 grid((unsigned)S, (unsigned)rows);
+  k_softmax_split_part<kSplitBlock, kSplitU, ALG, 0><<<grid, kSplitBlock, 0, st>>>(x, ldx, V, ch, rec);
+  osmx_host::count_launch();
+  if (ALG == osmx_host::kSafe) {
+    k_softmax_split_part<kSplitBlock, kSplitU, ALG, 1><<<grid, kSplitBlock, 0, st>>>(x, ldx, V, ch, rec);
+    osmx_host::count_launch();
+  }
+  k_softmax_split_scale<kSplitBlock, kSplitU, ALG><<<grid, kSplitBlock, 0, st>>>(x, ldx, y, ldy, V, ch, rec, ws);
+  osmx_host::count_launch();
+  return cudaGetLastError();
+}
+
+template <int ALG>
+cudaError_t launch_alg(const float* x, long long ldx, float* y, long long ldy, long long rows,
+                       long long V, void* ws, cudaStream_t st) {
+  const auto& tn = osmx_host::tuning();
+  int shape = tn.shape;
+  if (shape == osmx_host::kShapeAuto) {
+    if (V <= tn.resident_max_v)
+      shape = osmx_host::kShapeResident;
+    else if (rows >= 2LL * osmx_host::num_sms())
+      shape = osmx_host::kShapeStream;
+    else
+      shape = osmx_host::kShapeSplit;
+  }
+  if (shape == osmx_host::kShapeResident && V > 16384) shape = osmx_host::kShapeStream;
+  if (shape == osmx_host::kShapeResident) {
+    const bool vec = (V % 4 == 0) && (ldx % 4 == 0) && (ldy % 4 == 0) &&
+                     ((reinterpret_cast<uintptr_t>(x) & 15u) == 0) &&
+                     ((reinterpret_cast<uintptr_t>(y) & 15u) == 0);
+    return dispatch_resident<ALG>(vec, x, ldx, y, ldy, rows, V, ws, st);
+  }
+  if (shape == osmx_host::kShapeSplit) return run_split<ALG>(x, ldx, y, ldy, rows, V, ws, st);
+  return run_stream<ALG>(x, ldx, y, ldy, rows, V, ws, st);
+}
+
+}  // namespace

@@ -1,0 +1,128 @@
+// stream.cuh -- coalesced, 128-bit, unrolled streaming of one row segment by
+// a group of G threads (G = a sub-warp, a warp, or the whole CTA).
+//
+// A segment [p, p+n) is split into
+//   head : 0..3 scalar elements up to the first 16-byte boundary,
+//   body : nvec float4s, group-strided (thread t takes t, t+G, ...), U in
+//          flight per thread,
+//   tail : 0..3 scalar elements.
+// Each thread therefore sees its own elements in strictly increasing index
+// order (head < body < tail), which is what the strict-'>' top-K insertion
+// needs to reproduce the reference's tie order (topk.hpp:34-44).
+#pragma once
+
+#include "common.cuh"
+
+namespace osmx_dev {
+
+struct Seg {
+  const float* p;
+  long long n;
+  int head;        // scalar elements before the first aligned float4
+  long long nvec;  // aligned float4s
+  int tail;        // scalar elements after the body
+};
+
+__device__ __forceinline__ Seg make_seg(const float* p, long long n) {
+  Seg s;
+  s.p = p;
+  s.n = n;
+  const unsigned mis = static_cast<unsigned>(reinterpret_cast<uintptr_t>(p) & 15u);
+  long long h = mis ? (16 - mis) >> 2 : 0;  // float* is 4-byte aligned
+  if (h > n) h = n;
+  s.head = static_cast<int>(h);
+  s.nvec = (n - h) >> 2;
+  s.tail = static_cast<int>(n - h - 4 * s.nvec);
+  return s;
+}
+
+// Element index of component c of body float4 q.
+__device__ __forceinline__ long long body_index(const Seg& s, long long q, int c) {
+  return s.head + 4 * q + c;
+}
+
+// Visit every element of the segment once:
+//   f1(x, j)                    scalar element j
+//   fb(v[U], q0, cnt)           cnt (<= U) float4s at body indices q0 + u*G
+// LAST selects the evict-first load flavour (final read of the data).
+template <int G, int U, bool LAST, class F1, class FB>
+__device__ __forceinline__ void stream_seg(const Seg& s, int t, F1&& f1, FB&& fb) {
+  if (t < s.head) f1(LAST ? ld_f1_last(s.p + t) : ld_f1(s.p + t), (long long)t);
+  const float* b = s.p + s.head;
+  long long q = t;
+  for (; q + (long long)(U - 1) * G < s.nvec; q += (long long)U * G) {
+    float4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = LAST ? ld_f4_last(b + 4 * (q + (long long)u * G)) : ld_f4(b + 4 * (q + (long long)u * G));
+    fb(v, q, U);
+  }
+  if (q < s.nvec) {
+    float4 v[U];
+    int cnt = 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long qq = q + (long long)u * G;
+      if (qq < s.nvec) {
+        v[u] = LAST ? ld_f4_last(b + 4 * qq) : ld_f4(b + 4 * qq);
+        cnt = u + 1;
+      } else {
+        v[u] = make_float4(kNegInf, kNegInf, kNegInf, kNegInf);
+      }
+    }
+    fb(v, q, cnt);
+  }
+  if (t < s.tail) {
+    const long long j = s.head + 4 * s.nvec + t;
+    f1(LAST ? ld_f1_last(s.p + j) : ld_f1(s.p + j), j);
+  }
+}
+
+// Same traversal, writing one output per element (y has the same alignment
+// phase as x only when ldx == ldy; the output pointer is aligned
+// independently, falling back to scalar stores when phases differ).
+template <int G, int U, class FMAP>
+__device__ __forceinline__ void map_seg(const Seg& s, float* __restrict__ y, int t, FMAP&& f) {
+  const bool same_phase =
+      ((reinterpret_cast<uintptr_t>(y) & 15u) == (reinterpret_cast<uintptr_t>(s.p) & 15u));
+  if (t < s.head) st_f1(y + t, f(ld_f1_last(s.p + t)));
+  const float* b = s.p + s.head;
+  float* yb = y + s.head;
+  long long q = t;
+  for (; q + (long long)(U - 1) * G < s.nvec; q += (long long)U * G) {
+    float4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = ld_f4_last(b + 4 * (q + (long long)u * G));
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      float4 o = make_float4(f(v[u].x), f(v[u].y), f(v[u].z), f(v[u].w));
+      float* dst = yb + 4 * (q + (long long)u * G);
+      if (same_phase) {
+        st_f4(dst, o);
+      } else {
+        st_f1(dst, o.x);
+        st_f1(dst + 1, o.y);
+        st_f1(dst + 2, o.z);
+        st_f1(dst + 3, o.w);
+      }
+    }
+  }
+  for (; q < s.nvec; q += G) {
+    float4 v = ld_f4_last(b + 4 * q);
+    float4 o = make_float4(f(v.x), f(v.y), f(v.z), f(v.w));
+    float* dst = yb + 4 * q;
+    if (same_phase) {
+      st_f4(dst, o);
+    } else {
+      st_f1(dst, o.x);
+      st_f1(dst + 1, o.y);
+      st_f1(dst + 2, o.z);
+      st_f1(dst + 3, o.w);
+    }
+  }
+  if (t < s.tail) {
+    const long long j = s.head + 4 * s.nvec + t;
+    st_f1(y + j, f(ld_f1_last(s.p + j)));
+  }
+}
+
+}  // namespace osmx_dev

@@ -1,0 +1,513 @@
+// topk_impl.cuh -- batched top-K kernels for sm_100a.
+//
+// Replaces the reference's
+//   online_softmax_topk_kernel      kernels.hpp:108-125  (Alg. 4: ONE access
+//                                   per element; (m,d) and the top-K of the
+//                                   raw logits in the same pass)
+//   topk_kernel / topk_of           kernels.hpp:72-83, topk.cpp:20-28
+//   safe_softmax_fused_topk_kernel  kernels.hpp:87-104 (3 passes, selection
+//                                   on float(e^(x-m)/d))
+// The unfused pipelines (safe_softmax_then_topk, topk.cpp:30-35, and the
+// online->TopK comparator of the north star) are a softmax kernel followed
+// by the topk_of kernel here.
+//
+// Selection is exact: per-thread register lists insert with the reference's
+// strict '>' (topk.hpp:37-43) over elements seen in increasing index order,
+// and every merge level (warp, CTA, split chunk, GPU) uses the total order
+// (value desc, index asc) of oracle.cpp:48-51.  Indices are int64 on output
+// (topk.hpp:16).
+#pragma once
+#include <algorithm>
+
+#include "common.cuh"
+#include "internal.hpp"
+#include "stream.cuh"
+
+using namespace osmx_dev;
+
+namespace {
+
+enum Mode : int { kModeFused = 0, kModeTopkOf = 1, kModeSafe = 2 };
+
+// ----------------------------------------------------- record (chunk) --
+// Shared by the split path and the cross-GPU combine:
+//   float m, d, mn; int k; float v[k] (8-byte padded); int64 idx[k]
+struct RecHdr {
+  float m;
+  float d;
+  float mn;  // min of the slice (or NaN when a non-finite value was seen)
+  int k;
+};
+__host__ __device__ inline size_t rec_vals_off() { return sizeof(RecHdr); }
+__host__ __device__ inline size_t rec_idx_off(int k) { return sizeof(RecHdr) + ((size_t)(4 * k + 7) / 8) * 8; }
+__host__ __device__ inline size_t rec_bytes_(int k) { return ((rec_idx_off(k) + 8 * (size_t)k) + 15) / 16 * 16; }
+
+// --------------------------------------------------- per-thread pass --
+// State of one thread over the elements it owns: (m, d), min / check,
+// and the top list.  FUSED: list over raw x + online (m,d).  TOPK_OF: list
+// over x + finiteness check.  SAFE (select pass): list over p.
+template <int KC, int U, int MODE, int G>
+struct Pass {
+  TopList<KC> L;
+  float m = kNegInf, d = 0.0f, mn = -kNegInf, chk = 0.0f;
+  float M = 0.0f, R = 0.0f;  // SAFE select pass: row max and 1/d
+
+  __device__ __forceinline__ void scalar(float v, int j, int k) {
+    if constexpr (MODE == kModeFused) {
+      mn = fminf(mn, v);
+      if (v > m) {
+        d = d * exp_sub(m, v) + 1.0f;
+        m = v;
+      } else {
+        d += exp_sub(v, m);
+      }
+      L.offer(v, j);
+    } else if constexpr (MODE == kModeTopkOf) {
+      chk = fmaf(v, 0.0f, chk);  // NaN iff some element was inf / NaN
+      L.offer(v, j);
+    } else {
+      L.offer(expf(v - M) * R, j);
+    }
+  }
+  __device__ __forceinline__ void batch(const Seg& s, float4 (&v)[U], long long q0, int cnt, int k) {
+    if constexpr (MODE == kModeFused) {
+      float bm = kNegInf, bn = -kNegInf;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        bm = fmaxf(bm, fmaxf(fmaxf(v[u].x, v[u].y), fmaxf(v[u].z, v[u].w)));
+        if (u < cnt) bn = fminf(bn, fminf(fminf(v[u].x, v[u].y), fminf(v[u].z, v[u].w)));
+      }
+      mn = fminf(mn, bn);
+      if (bm > m) {
+        d *= exp_sub(m, bm);
+        m = bm;
+      }
+      float sum = 0.0f;
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        sum += (exp_sub(v[u].x, m) + exp_sub(v[u].y, m)) + (exp_sub(v[u].z, m) + exp_sub(v[u].w, m));
+      d += sum;
+      if (bm > L.thr()) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (u >= cnt) break;  // padding of the last batch is never offered
+          const int j = (int)body_index(s, q0 + (long long)u * G, 0);
+          L.offer(v[u].x, j);
+          L.offer(v[u].y, j + 1);
+          L.offer(v[u].z, j + 2);
+          L.offer(v[u].w, j + 3);
+        }
+      }
+    } else if constexpr (MODE == kModeTopkOf) {
+      float bm = kNegInf;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        bm = fmaxf(bm, fmaxf(fmaxf(v[u].x, v[u].y), fmaxf(v[u].z, v[u].w)));
+        if (u < cnt) {
+          chk = fmaf(v[u].x, 0.0f, chk);
+          chk = fmaf(v[u].y, 0.0f, chk);
+          chk = fmaf(v[u].z, 0.0f, chk);
+          chk = fmaf(v[u].w, 0.0f, chk);
+        }
+      }
+      if (bm > L.thr()) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (u >= cnt) break;  // padding of the last batch is never offered
+          const int j = (int)body_index(s, q0 + (long long)u * G, 0);
+          L.offer(v[u].x, j);
+          L.offer(v[u].y, j + 1);
+          L.offer(v[u].z, j + 2);
+          L.offer(v[u].w, j + 3);
+        }
+      }
+    } else {
+      // p is monotone in x for a fixed row (M, R): filter on x first.
+      float bm = kNegInf;
+#pragma unroll
+      for (int u = 0; u < U; ++u) bm = fmaxf(bm, fmaxf(fmaxf(v[u].x, v[u].y), fmaxf(v[u].z, v[u].w)));
+      if (expf(bm - M) * R >= L.thr()) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (u >= cnt) break;  // padding of the last batch is never offered
+          const int j = (int)body_index(s, q0 + (long long)u * G, 0);
+          L.offer(expf(v[u].x - M) * R, j);
+          L.offer(expf(v[u].y - M) * R, j + 1);
+          L.offer(expf(v[u].z - M) * R, j + 2);
+          L.offer(expf(v[u].w - M) * R, j + 3);
+        }
+      }
+    }
+  }
+};
+
+// Safe fused top-K needs the row max and 1/d before the selection pass.
+template <int G, int U>
+__device__ __forceinline__ void safe_max_min(const Seg& s, int t, float& m, float& mn) {
+  stream_seg<G, U, false>(
+      s, t,
+      [&](float v, long long) {
+        m = fmaxf(m, v);
+        mn = fminf(mn, v);
+        if (v != v) mn = v;
+      },
+      [&](float4 (&v)[U], long long, int cnt) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          m = fmaxf(m, fmaxf(fmaxf(v[u].x, v[u].y), fmaxf(v[u].z, v[u].w)));
+          if (u < cnt) mn = fminf(mn, fminf(fminf(v[u].x, v[u].y), fminf(v[u].z, v[u].w)));
+        }
+      });
+}
+template <int G, int U>
+__device__ __forceinline__ float safe_sum(const Seg& s, int t, float M) {
+  float d = 0.0f;
+  stream_seg<G, U, false>(
+      s, t, [&](float v, long long) { d += exp_sub(v, M); },
+      [&](float4 (&v)[U], long long, int) {
+        float sum = 0.0f;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          sum += (exp_sub(v[u].x, M) + exp_sub(v[u].y, M)) + (exp_sub(v[u].z, M) + exp_sub(v[u].w, M));
+        d += sum;
+      });
+  return d;
+}
+
+template <int G, int U, int KC, int MODE>
+__device__ __forceinline__ void run_pass(Pass<KC, U, MODE, G>& P, const Seg& s, int t, int k) {
+  stream_seg<G, U, MODE == kModeSafe>(
+      s, t, [&](float v, long long j) { P.scalar(v, (int)j, k); },
+      [&](float4 (&v)[U], long long q0, int cnt) { P.batch(s, v, q0, cnt, k); });
+}
+
+// Cross-warp merge for a CTA-wide group: each warp's k winners go to smem,
+// warp 0 merges them.  sv/si hold NW*KC entries.
+template <int NW, int KC, class Sink>
+__device__ __forceinline__ void cta_merge(TopList<KC>& L, int k, float* sv, int* si, Sink&& sink) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  L.normalize(k);
+  group_merge<32>(L, k, [&](int r, float v, int i) {
+    if (l == 0) {
+      sv[w * KC + r] = v;
+      si[w * KC + r] = i;
+    }
+  });
+  __syncthreads();
+  if (w == 0) {
+    TopList<KC> M;
+    M.init_empty();
+    if (l < NW) {
+#pragma unroll
+      for (int r = 0; r < KC; ++r)
+        if (r < k) {
+          M.v[r] = sv[l * KC + r];
+          M.i[r] = si[l * KC + r];
+        }
+    }
+    group_merge<32>(M, k, sink);
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------- row kernel --
+// G threads per row (G == 32: warp per row, BLOCK/32 rows per CTA; G ==
+// BLOCK: CTA per row).  Rows are visited grid-stride.
+template <int G, int BLOCK, int KC, int MODE, int U>
+__global__ void __launch_bounds__(BLOCK)
+    k_topk_rows(const float* __restrict__ x, long long ldx, long long rows, long long V, int k,
+                float* __restrict__ vals, long long* __restrict__ idx, void* ws) {
+  constexpr int NW = BLOCK / 32;
+  constexpr int RPC = BLOCK / G;
+  __shared__ float smf[2 * NW];
+  __shared__ float sv[NW * KC];
+  __shared__ int si[NW * KC];
+  const int t = threadIdx.x % G;
+  const long long nrow_groups = (rows + RPC - 1) / RPC;
+  for (long long rg = blockIdx.x; rg < nrow_groups; rg += gridDim.x) {
+    const long long row = rg * RPC + threadIdx.x / G;
+    const bool live = row < rows;
+    const Seg s = make_seg(x + (live ? row : 0) * ldx, live ? V : 0);
+    Pass<KC, U, MODE, G> P;
+    P.L.init(k);
+    bool bad = false;
+    float outM = 0.0f, outR = 1.0f;
+    if constexpr (MODE == kModeSafe) {
+      float m = kNegInf, mn = -kNegInf;
+      safe_max_min<G, U>(s, t, m, mn);
+      float M, MN;
+      if constexpr (G == 32) {
+        M = group_max<32>(m);
+        MN = group_min<32>(mn);
+      } else {
+        M = cta_max<NW>(m, smf);
+        MN = cta_min<NW>(mn, smf);
+      }
+      float d = safe_sum<G, U>(s, t, M);
+      if constexpr (G == 32)
+        d = group_sum<32>(d);
+      else
+        d = cta_sum<NW>(d, smf);
+      P.M = M;
+      P.R = __frcp_rn(d);
+      bad = !(d == d) || !isfinite(M) || !(MN == MN) || MN == kNegInf;
+    }
+    run_pass<G, U, KC, MODE>(P, s, t, k);
+    if constexpr (MODE == kModeFused) {
+      MD tot;
+      float MN;
+      if constexpr (G == 32) {
+        tot = md_group_reduce<32>(MD{P.m, P.d});
+        MN = group_min<32>(P.mn);
+      } else {
+        tot = md_cta_reduce<NW>(MD{P.m, P.d}, smf);
+        MN = cta_min<NW>(P.mn, smf);
+      }
+      outM = tot.m;
+      outR = __frcp_rn(tot.d);
+      bad = !(tot.d == tot.d) || !isfinite(tot.m) || MN == kNegInf;
+    } else if constexpr (MODE == kModeTopkOf) {
+      float c;
+      if constexpr (G == 32)
+        c = group_sum<32>(P.chk);
+      else
+        c = cta_sum<NW>(P.chk, smf);
+      bad = !(c == c);
+    }
+    auto sink = [&](int r, float v, int i) {
+      if (live && (int)(threadIdx.x & 31) == (r & 31)) {
+        float out = v;
+        if constexpr (MODE == kModeFused) out = expf(v - outM) * outR;  // kernels.hpp:122
+        vals[row * k + r] = out;
+        idx[row * k + r] = (long long)i;
+      }
+    };
+    if constexpr (G == 32) {
+      P.L.normalize(k);
+      group_merge<32>(P.L, k, sink);
+    } else {
+      cta_merge<NW>(P.L, k, sv, si, sink);
+    }
+    if (live && bad && t == 0) flag_bad_row(ws, row);
+  }
+}
+
+// --------------------------------------------------------- split part --
+// grid (S, rows): CTA (c, row) reduces chunk c of the row into a record.
+// col0 shifts the global index (V-split across GPUs).  For kModeSafe the
+// row (M, 1/d) come from the softmax split records (srec, phase 0/1).
+struct SRecView {
+  float m;
+  float mn;
+  double d;
+};
+template <int BLOCK, int KC, int MODE, int U>
+__global__ void __launch_bounds__(BLOCK)
+    k_topk_split_part(const float* __restrict__ x, long long ldx, long long V, long long chunk,
+                      int k, long long col0, char* __restrict__ rec, const SRecView* __restrict__ srec) {
+  constexpr int NW = BLOCK / 32;
+  __shared__ float smf[2 * NW];
+  __shared__ float sv[NW * KC];
+  __shared__ int si[NW * KC];
+  const int S = gridDim.x;
+  const long long row = blockIdx.y;
+  const long long c0 = (long long)blockIdx.x * chunk;
+  const long long n = std::min(chunk, V - c0);
+  const Seg s = make_seg(x + row * ldx + c0, n);
+  const int t = threadIdx.x;
+  Pass<KC, U, MODE, BLOCK> P;
+  P.L.init(k);
+  float safe_mn = 0.0f;
+  if constexpr (MODE == kModeSafe) {
+    const SRecView* rr = srec + row * S;
+    float M = kNegInf, d = 0.0f, mn = -kNegInf;
+    for (int i = t; i < S; i += BLOCK) {
+      M = fmaxf(M, rr[i].m);
+      mn = fminf(mn, rr[i].mn);
+      if (rr[i].mn != rr[i].mn) mn = kNegInf;
+      d += (float)rr[i].d;
+    }
+    M = cta_max<NW>(M, smf);
+    mn = cta_min<NW>(mn, smf);
+    d = cta_sum<NW>(d, smf);
+    P.M = M;
+    P.R = __frcp_rn(d);
+    // poison the record when the row holds a non-finite value
+    if (!(d == d) || !isfinite(M) || mn == kNegInf) safe_mn = __int_as_float(0x7fffffff);
+  }
+  run_pass<BLOCK, U, KC, MODE>(P, s, t, k);
+  RecHdr h{0.0f, 0.0f, 0.0f, k};
+  if constexpr (MODE == kModeFused) {
+    MD tot = md_cta_reduce<NW>(MD{P.m, P.d}, smf);
+    h.m = tot.m;
+    h.d = tot.d;
+    h.mn = cta_min<NW>(P.mn, smf);
+  } else if constexpr (MODE == kModeTopkOf) {
+    const float c = cta_sum<NW>(P.chk, smf);
+    h.mn = (c == c) ? 0.0f : c;
+    h.m = kNegInf;
+  } else {
+    h.m = kNegInf;
+    h.mn = safe_mn;
+  }
+  char* my = rec + ((size_t)row * S + blockIdx.x) * rec_bytes_(k);
+  float* rv = reinterpret_cast<float*>(my + rec_vals_off());
+  long long* ri = reinterpret_cast<long long*>(my + rec_idx_off(k));
+  const long long base = c0 + col0;
+  cta_merge<NW>(P.L, k, sv, si, [&](int r, float v, int i) {
+    if ((int)(threadIdx.x & 31) == (r & 31)) {
+      rv[r] = v;
+      ri[r] = i < 0 ? -1LL : (long long)i + base;
+    }
+  });
+  if (t == 0) *reinterpret_cast<RecHdr*>(my) = h;
+}
+
+// ------------------------------------------------------------- combine --
+// One warp per row merges n records (rank / chunk order).  Writes the
+// merged record (out_rec, optional) and the final (vals, idx) (optional).
+// mode: kModeFused outputs e^(u - M)/D; others output the values as is.
+template <int KC>
+__global__ void __launch_bounds__(32)
+    k_topk_combine(const char* __restrict__ rec, int n, int k, int mode, char* __restrict__ out_rec,
+                   float* __restrict__ vals, long long* __restrict__ idx, long long row_base,
+                   void* ws) {
+  const long long row = blockIdx.x;
+  const int l = threadIdx.x;
+  const size_t rb = rec_bytes_(k);
+  const char* rr = rec + (size_t)row * n * rb;
+  MD a = md_identity();
+  float mn = -kNegInf;
+  bool nan_seen = false;
+  TopList<KC, long long> L;
+  L.init(k);
+  for (int c = l; c < n; c += 32) {
+    const char* my = rr + (size_t)c * rb;
+    const RecHdr h = *reinterpret_cast<const RecHdr*>(my);
+    a = md_merge(a, MD{h.m, h.d});
+    if (h.mn != h.mn) nan_seen = true;
+    mn = fminf(mn, h.mn);
+    const float* rv = reinterpret_cast<const float*>(my + rec_vals_off());
+    const long long* ri = reinterpret_cast<const long long*>(my + rec_idx_off(k));
+    for (int r = 0; r < k; ++r) L.offer_ordered(rv[r], ri[r]);
+  }
+  a = md_group_reduce<32>(a);
+  mn = group_min<32>(mn);
+  nan_seen = __any_sync(0xffffffffu, nan_seen);
+  bool bad;
+  if (mode == kModeFused)
+    bad = !(a.d == a.d) || !isfinite(a.m) || mn == kNegInf || nan_seen;
+  else
+    bad = nan_seen;
+  const float R = __frcp_rn(a.d);
+  char* orec = out_rec ? out_rec + (size_t)row * rb : nullptr;
+  L.normalize(k);
+  group_merge<32>(L, k, [&](int r, float v, long long i) {
+    if ((l & 31) == (r & 31)) {
+      if (orec) {
+        reinterpret_cast<float*>(orec + rec_vals_off())[r] = v;
+        reinterpret_cast<long long*>(orec + rec_idx_off(k))[r] = i;
+      }
+      if (vals) {
+        vals[row * k + r] = mode == kModeFused ? expf(v - a.m) * R : v;
+        idx[row * k + r] = i;
+      }
+    }
+  });
+  if (l == 0) {
+    if (orec) *reinterpret_cast<RecHdr*>(orec) = RecHdr{a.m, a.d, nan_seen ? __int_as_float(0x7fffffff) : mn, k};
+    if (bad && ws) flag_bad_row(ws, row_base + row);
+  }
+}
+
+// ------------------------------------------------------------ launchers --
+
+template <int KC, int MODE>
+cudaError_t run_rows(const float* x, long long ldx, long long rows, long long V, int k, float* vals,
+                     long long* idx, void* ws, cudaStream_t st) {
+  const int sms = osmx_host::num_sms();
+  int threads = osmx_host::tuning().topk_threads;
+  if (V <= 2048 && threads == 0) {
+    constexpr int RPC = 256 / 32;
+    const long long groups = (rows + RPC - 1) / RPC;
+    const long long grid = std::min<long long>(groups, 1LL << 30);
+    k_topk_rows<32, 256, KC, MODE, 2><<<(unsigned)grid, 256, 0, st>>>(x, ldx, rows, V, k, vals, idx, ws);
+  } else {
+    (void)sms;
+    const long long grid = std::min<long long>(rows, 1LL << 30);
+    k_topk_rows<256, 256, KC, MODE, 4><<<(unsigned)grid, 256, 0, st>>>(x, ldx, rows, V, k, vals, idx, ws);
+  }
+  osmx_host::count_launch();
+  return cudaGetLastError();
+}
+
+constexpr int kSplitBlock = 512;
+constexpr int kSplitU = 4;
+
+long long topk_split_chunk(long long rows, long long V) {
+  long long ch = osmx_host::tuning().split_chunk;
+  if (ch <= 0) {
+    const long long target = 4LL * osmx_host::num_sms();
+    long long per_row = std::max<long long>(1, target / std::max<long long>(rows, 1));
+    ch = (V + per_row - 1) / per_row;
+    ch = std::max<long long>(ch, 32768);
+  }
+  return (ch + 15) / 16 * 16;
+}
+
+template <int KC, int MODE>
+cudaError_t run_split(const float* x, long long ldx, long long rows, long long V, int k, float* vals,
+                      long long* idx, void* ws, cudaStream_t st, long long col0, char* out_rec) {
+  const long long ch = topk_split_chunk(rows, V);
+  const long long S = (V + ch - 1) / ch;
+  char* base = static_cast<char*>(ws) + kWsHeader;
+  char* rec = base;
+  const SRecView* srec = nullptr;
+  if constexpr (MODE == kModeSafe) {
+    // Row max / normalizer from the softmax split phases.
+    srec = reinterpret_cast<const SRecView*>(base);
+    rec = base + ((size_t)(rows * S) * sizeof(SRecView) + 255) / 256 * 256;
+    cudaError_t e = osmx_host::launch_safe_split_stats(x, ldx, rows, V, ch, const_cast<SRecView*>(srec), st);
+    if (e != cudaSuccess) return e;
+  }
+  dim3 grid((unsigned)S, (unsigned)rows);
+  k_topk_split_part<kSplitBlock, KC, MODE, kSplitU><<<grid, kSplitBlock, 0, st>>>(x, ldx, V, ch, k, col0, rec, srec);
+  osmx_host::count_launch();
+  k_topk_combine<KC><<<(unsigned)rows, 32, 0, st>>>(rec, (int)S, k, MODE, out_rec, vals, idx, 0, ws);
+  osmx_host::count_launch();
+  return cudaGetLastError();
+}
+
+template <int MODE>
+cudaError_t dispatch_mode(const float* x, long long ldx, long long rows, long long V, int k, float* vals,
+                          long long* idx, void* ws, cudaStream_t st, bool split, long long col0,
+                          char* out_rec) {
+#define OSMX_KC_CASE(KC)                                                               \
+  if (split) return run_split<KC, MODE>(x, ldx, rows, V, k, vals, idx, ws, st, col0, out_rec); \
+  return run_rows<KC, MODE>(x, ldx, rows, V, k, vals, idx, ws, st);
+  if (k <= 1) { OSMX_KC_CASE(1) }
+  if (k <= 5) { OSMX_KC_CASE(5) }
+  if (k <= 8) { OSMX_KC_CASE(8) }
+  if (k <= 16) { OSMX_KC_CASE(16) }
+  { OSMX_KC_CASE(32) }
+#undef OSMX_KC_CASE
+}
+
+bool topk_uses_split(long long rows, long long V) {
+  const auto& tn = osmx_host::tuning();
+  if (tn.shape == osmx_host::kShapeSplit) return true;
+  if (tn.shape != osmx_host::kShapeAuto) return false;
+  return V > 65536 && rows < 2LL * osmx_host::num_sms();
+}
+
+template <int KC>
+cudaError_t combine_kc(const void* records, int n, int k, void* out_record, float* vals,
+                       long long* idx, void* ws, cudaStream_t st) {
+  k_topk_combine<KC><<<1, 32, 0, st>>>(static_cast<const char*>(records), n, k,
+                                       kModeFused,
+                                       static_cast<char*>(out_record), vals, idx, 0, ws);
+  osmx_host::count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace

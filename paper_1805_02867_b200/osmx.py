@@ -1,0 +1,454 @@
+"""Python host API mirroring the reference ``osmx`` library, backed by the
+sm_100a kernels through the C-ABI (include/osmx_b200.h).
+
+Two layers:
+
+* **Reference-shaped functions** (same names, argument meaning and error
+  behaviour as ``proj/include/osmx/{softmax,topk,normalizer}.hpp``): a 1-D
+  float vector in, a fresh result out.  They run the batched host-buffer
+  entry points (``osmx_*_host``) -- copy in, kernel, copy out -- and accept a
+  2-D array as a batch of rows.
+
+    naive_softmax(x)             softmax.hpp:17   (Alg. 1)
+    safe_softmax(x)              softmax.hpp:22   (Alg. 2)
+    online_softmax(x)            softmax.hpp:28   (Alg. 3)
+    topk_of(values, k)           topk.hpp:54
+    safe_softmax_then_topk(x, k) topk.hpp:58
+    safe_softmax_fused_topk(x,k) topk.hpp:63
+    online_softmax_topk(x, k)    topk.hpp:68      (Alg. 4)
+    run_normalizer(x)            normalizer.hpp:61-67
+    run_normalizer_chunked(x,c)  normalizer.hpp:73-85
+
+  Errors are the reference's exception types (error.hpp:8-25), all
+  subclasses of ValueError as the reference's derive from
+  std::invalid_argument.
+
+* **Batched device functions** on torch CUDA tensors (``softmax``,
+  ``softmax_topk``, ``topk``, ``normalizer``, and the V-split record
+  functions), stream-ordered on torch's current stream.
+
+There is no CPU fallback: every call goes through ``libosmx_b200.so``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import NamedTuple
+
+import numpy as np
+
+from . import _lib
+from ._lib import load
+
+# ------------------------------------------------------------------ errors --
+
+
+class OsmxError(Exception):
+    """Base of the non-argument failures (CUDA errors, unsupported k)."""
+
+
+class EmptyInputError(ValueError):
+    """empty_input_error (error.hpp:8-10)."""
+
+    def __init__(self, msg: str = "empty input vector"):
+        super().__init__(msg)
+
+
+class NonFiniteError(ValueError):
+    """non_finite_error (error.hpp:13-15).  ``row`` is the first bad row."""
+
+    def __init__(self, msg: str = "non-finite input element", row: int = -1):
+        super().__init__(msg)
+        self.row = row
+
+
+class InvalidKError(ValueError):
+    """invalid_k_error (error.hpp:18-20): k outside [1, V]."""
+
+    def __init__(self, msg: str = "k must satisfy 1 <= k <= input size"):
+        super().__init__(msg)
+
+
+class InvalidChunkError(ValueError):
+    """invalid_chunk_error (error.hpp:23-25)."""
+
+    def __init__(self, msg: str = "chunk length must be >= 1"):
+        super().__init__(msg)
+
+
+class CudaError(OsmxError):
+    pass
+
+
+class UnsupportedError(OsmxError):
+    pass
+
+
+def _raise(status: int, row: int = -1) -> None:
+    if status == _lib.OK:
+        return
+    if status == _lib.ERR_EMPTY:
+        raise EmptyInputError()
+    if status == _lib.ERR_NON_FINITE:
+        raise NonFiniteError(row=row)
+    if status == _lib.ERR_INVALID_K:
+        raise InvalidKError()
+    if status == _lib.ERR_INVALID_CHUNK:
+        raise InvalidChunkError()
+    if status == _lib.ERR_CUDA:
+        raise CudaError(load().osmx_last_cuda_error().decode())
+    if status == _lib.ERR_UNSUPPORTED:
+        raise UnsupportedError(f"k above {_lib.MAX_K} is not supported on the device path")
+    raise ValueError(_lib.status_string(status))
+
+
+class TopkResult(NamedTuple):
+    """topk_result (topk.hpp:14-17): values sorted non-increasing, int64 indices."""
+
+    values: np.ndarray
+    indices: np.ndarray
+
+
+class NormState(NamedTuple):
+    """norm_state (normalizer.hpp:24-46): (max, sum of e^(x - max))."""
+
+    max: float
+    sum: float
+
+
+ALGS = {
+    "naive": _lib.NAIVE_SOFTMAX,
+    "safe": _lib.SAFE_SOFTMAX,
+    "online": _lib.ONLINE_SOFTMAX,
+    "safe_unfused": _lib.SAFE_SOFTMAX_UNFUSED_TOPK,
+    "safe_fused": _lib.SAFE_SOFTMAX_FUSED_TOPK,
+    "online_fused": _lib.ONLINE_SOFTMAX_FUSED_TOPK,
+    "online_unfused": _lib.ONLINE_SOFTMAX_UNFUSED_TOPK,
+}
+
+_device = 0
+
+
+def set_device(device: int) -> None:
+    """CUDA device used by the host-buffer (reference-shaped) functions."""
+    global _device
+    _device = int(device)
+
+
+# ------------------------------------------------ reference-shaped (host) --
+
+def _as_rows(x) -> tuple[np.ndarray, bool]:
+    a = np.ascontiguousarray(np.asarray(x, dtype=np.float32))
+    if a.ndim == 1:
+        return a.reshape(1, -1), True
+    if a.ndim != 2:
+        raise ValueError("expected a 1-D vector or a 2-D batch of rows")
+    return a, False
+
+
+def _softmax_host(alg: int, x) -> np.ndarray:
+    a, single = _as_rows(x)
+    rows, V = a.shape
+    if V == 0:
+        raise EmptyInputError()
+    y = np.empty_like(a)
+    bad = C.c_int64(-1)
+    st = load().osmx_softmax_host(alg, a.ctypes.data, rows, V, y.ctypes.data, _device, C.byref(bad))
+    _raise(st, bad.value)
+    return y[0] if single else y
+
+
+def _topk_host(alg: int | None, x, k: int) -> TopkResult:
+    a, single = _as_rows(x)
+    rows, V = a.shape
+    if V == 0:
+        raise EmptyInputError()
+    k = int(k)
+    if k < 1 or k > V:
+        raise InvalidKError()
+    vals = np.empty((rows, k), np.float32)
+    idx = np.empty((rows, k), np.int64)
+    bad = C.c_int64(-1)
+    if alg is None:
+        st = load().osmx_topk_host(a.ctypes.data, rows, V, k, vals.ctypes.data, idx.ctypes.data, _device,
+                                   C.byref(bad))
+    else:
+        st = load().osmx_softmax_topk_host(alg, a.ctypes.data, rows, V, k, vals.ctypes.data, idx.ctypes.data,
+                                           _device, C.byref(bad))
+    _raise(st, bad.value)
+    if single:
+        return TopkResult(vals[0], idx[0])
+    return TopkResult(vals, idx)
+
+
+def naive_softmax(x) -> np.ndarray:
+    """Alg. 1 (softmax.hpp:13-17): no overflow guard; Inf/NaN returned as is."""
+    return _softmax_host(_lib.NAIVE_SOFTMAX, x)
+
+
+def safe_softmax(x) -> np.ndarray:
+    """Alg. 2 (softmax.hpp:19-22): max, normalizer, outputs."""
+    return _softmax_host(_lib.SAFE_SOFTMAX, x)
+
+
+def online_softmax(x) -> np.ndarray:
+    """Alg. 3 (softmax.hpp:24-28): fused (max, normalizer) pass, then outputs."""
+    return _softmax_host(_lib.ONLINE_SOFTMAX, x)
+
+
+def topk_of(values, k: int) -> TopkResult:
+    """K largest values with indices, ties to the smaller index (topk.hpp:52-54)."""
+    return _topk_host(None, values, k)
+
+
+def safe_softmax_then_topk(x, k: int) -> TopkResult:
+    """safe_softmax then topk_of, materialising y (topk.hpp:56-58)."""
+    return _topk_host(_lib.SAFE_SOFTMAX_UNFUSED_TOPK, x, k)
+
+
+def safe_softmax_fused_topk(x, k: int) -> TopkResult:
+    """Three passes, selection on the on-the-fly probability (topk.hpp:60-63)."""
+    return _topk_host(_lib.SAFE_SOFTMAX_FUSED_TOPK, x, k)
+
+
+def online_softmax_topk(x, k: int) -> TopkResult:
+    """Alg. 4: one pass, (m, d) + top-K of the raw logits (topk.hpp:65-68)."""
+    return _topk_host(_lib.ONLINE_SOFTMAX_FUSED_TOPK, x, k)
+
+
+def online_softmax_then_topk(x, k: int) -> TopkResult:
+    """online_softmax then topk_of: the unfused comparator of the north star."""
+    return _topk_host(_lib.ONLINE_SOFTMAX_UNFUSED_TOPK, x, k)
+
+
+def _normalizer_host(x, chunk: int | None) -> NormState | tuple[np.ndarray, np.ndarray]:
+    import torch
+
+    a, single = _as_rows(x)
+    rows, V = a.shape
+    if V == 0:
+        raise EmptyInputError()
+    if chunk is not None and chunk == 0:
+        raise InvalidChunkError()
+    dev = torch.device("cuda", _device)
+    xt = torch.from_numpy(a).to(dev)
+    m, d = normalizer(xt, chunk=chunk or 0)
+    m, d = m.cpu().numpy(), d.cpu().numpy()
+    if single:
+        return NormState(float(m[0]), float(d[0]))
+    return m, d
+
+
+def run_normalizer(x):
+    """(max, sum e^(x-max)) of the vector (normalizer.hpp:60-67)."""
+    return _normalizer_host(x, None)
+
+
+def run_normalizer_chunked(x, chunk_len: int):
+    """Chunked normalizer (normalizer.hpp:69-85).  chunk_len == 0 raises
+    InvalidChunkError like the reference; the device evaluation order is the
+    CTA merge tree (the reference pins its equivalence,
+    test_normalizer.cpp:229-262)."""
+    if int(chunk_len) < 0:
+        raise InvalidChunkError()
+    return _normalizer_host(x, int(chunk_len))
+
+
+# ---------------------------------------------------- batched (device) -----
+
+class _Workspace:
+    """Per-device, grow-only workspace (zero-initialised header)."""
+
+    def __init__(self):
+        self.buf = {}
+
+    def get(self, nbytes: int, device, stream_ptr: int):
+        import torch
+
+        key = device.index if device.index is not None else 0
+        t = self.buf.get(key)
+        if t is None or t.numel() < nbytes:
+            t = torch.zeros(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+            self.buf[key] = t
+        return t
+
+
+_ws = _Workspace()
+
+
+def _stream_ptr(device) -> int:
+    import torch
+
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _check_tensor(x, name="x"):
+    import torch
+
+    if not isinstance(x, torch.Tensor) or not x.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor (the device path has no CPU fallback)")
+    if x.dtype != torch.float32:
+        raise TypeError(f"{name} must be float32")
+    if x.dim() == 1:
+        x = x.unsqueeze(0)
+    if x.dim() == 2 and x.shape[1] == 0:
+        raise EmptyInputError()
+    if x.dim() != 2 or (x.stride(1) != 1 and x.shape[1] > 1):
+        raise ValueError(f"{name} must be 1-D or 2-D with unit stride along V")
+    return x
+
+
+def check_status(ws, stream: int) -> None:
+    bad = C.c_int64(-1)
+    st = load().osmx_check_status(ws.data_ptr(), stream, C.byref(bad))
+    _raise(st, bad.value)
+
+
+def workspace(alg: int, rows: int, V: int, k: int, device):
+    nb = load().osmx_workspace_bytes(alg, rows, V, k)
+    return _ws.get(nb, device, _stream_ptr(device)), nb
+
+
+def softmax(x, alg: str = "online", out=None, check: bool = True):
+    """Batched softmax of every row of a CUDA float32 tensor (rows x V)."""
+    import torch
+
+    x2 = _check_tensor(x)
+    rows, V = x2.shape
+    if V == 0:
+        raise EmptyInputError()
+    a = ALGS[alg]
+    if out is None:
+        out = torch.empty_like(x2)
+    y = out if out.dim() == 2 else out.unsqueeze(0)
+    stream = _stream_ptr(x2.device)
+    ws, nb = workspace(a, rows, V, 0, x2.device)
+    st = load().osmx_softmax(a, x2.data_ptr(), x2.stride(0), y.data_ptr(), y.stride(0), rows, V, ws.data_ptr(),
+                             ws.numel(), stream)
+    _raise(st)
+    if check:
+        check_status(ws, stream)
+    return out if x.dim() == 2 else y[0]
+
+
+def softmax_topk(x, k: int, alg: str = "online_fused", check: bool = True, out=None):
+    """Batched softmax + top-K: returns (values rows x k, int64 indices rows x k)."""
+    import torch
+
+    x2 = _check_tensor(x)
+    rows, V = x2.shape
+    if V == 0:
+        raise EmptyInputError()
+    a = ALGS[alg]
+    if out is None:
+        vals = torch.empty((rows, max(k, 1)), dtype=torch.float32, device=x2.device)
+        idx = torch.empty((rows, max(k, 1)), dtype=torch.int64, device=x2.device)
+    else:
+        vals, idx = out
+    stream = _stream_ptr(x2.device)
+    ws, nb = workspace(a, rows, V, k, x2.device)
+    st = load().osmx_softmax_topk(a, x2.data_ptr(), x2.stride(0), rows, V, k, vals.data_ptr(), idx.data_ptr(),
+                                  ws.data_ptr(), ws.numel(), stream)
+    _raise(st)
+    if check:
+        check_status(ws, stream)
+    if x.dim() == 1:
+        return vals[0], idx[0]
+    return vals, idx
+
+
+def topk(v, k: int, check: bool = True):
+    """Batched topk_of over a CUDA float32 tensor of values."""
+    import torch
+
+    v2 = _check_tensor(v, "v")
+    rows, V = v2.shape
+    if V == 0:
+        raise EmptyInputError()
+    vals = torch.empty((rows, max(k, 1)), dtype=torch.float32, device=v2.device)
+    idx = torch.empty((rows, max(k, 1)), dtype=torch.int64, device=v2.device)
+    stream = _stream_ptr(v2.device)
+    ws, nb = workspace(7, rows, V, k, v2.device)
+    st = load().osmx_topk(v2.data_ptr(), v2.stride(0), rows, V, k, vals.data_ptr(), idx.data_ptr(), ws.data_ptr(),
+                          ws.numel(), stream)
+    _raise(st)
+    if check:
+        check_status(ws, stream)
+    if v.dim() == 1:
+        return vals[0], idx[0]
+    return vals, idx
+
+
+def normalizer(x, chunk: int = 0, check: bool = True):
+    """Batched (m, d) per row (float32 tensors)."""
+    import torch
+
+    x2 = _check_tensor(x)
+    rows, V = x2.shape
+    if V == 0:
+        raise EmptyInputError()
+    m = torch.empty(rows, dtype=torch.float32, device=x2.device)
+    d = torch.empty(rows, dtype=torch.float32, device=x2.device)
+    stream = _stream_ptr(x2.device)
+    ws, nb = workspace(8, rows, V, 0, x2.device)
+    st = load().osmx_normalizer(x2.data_ptr(), x2.stride(0), rows, V, chunk, m.data_ptr(), d.data_ptr(),
+                                ws.data_ptr(), ws.numel(), stream)
+    _raise(st)
+    if check:
+        check_status(ws, stream)
+    return m, d
+
+
+# ------------------------------------------------ V-split records (dist) ---
+
+def record_bytes(k: int) -> int:
+    return int(load().osmx_record_bytes(k))
+
+
+def slice_record(x_slice, col0: int, k: int):
+    """Record (m, d, top-k with global indices) of one row slice (uint8 tensor)."""
+    import torch
+
+    x1 = _check_tensor(x_slice)
+    if x1.shape[0] != 1:
+        raise ValueError("slice_record takes one row slice")
+    V = x1.shape[1]
+    rec = torch.empty(record_bytes(k), dtype=torch.uint8, device=x1.device)
+    stream = _stream_ptr(x1.device)
+    nb = load().osmx_workspace_bytes(9, 1, V, max(k, 1))
+    ws = _ws.get(nb, x1.device, stream)
+    st = load().osmx_slice_record(x1.data_ptr(), V, col0, k, rec.data_ptr(), ws.data_ptr(), ws.numel(), stream)
+    _raise(st)
+    return rec
+
+
+def records_combine(records, k: int, check: bool = True):
+    """Merge n records (n x record_bytes uint8 tensor, rank order).
+    Returns (vals[k], idx[k], merged_record)."""
+    import torch
+
+    n = records.shape[0]
+    out_rec = torch.empty(record_bytes(k), dtype=torch.uint8, device=records.device)
+    vals = torch.empty(max(k, 1), dtype=torch.float32, device=records.device)
+    idx = torch.empty(max(k, 1), dtype=torch.int64, device=records.device)
+    stream = _stream_ptr(records.device)
+    ws = _ws.get(256, records.device, stream)
+    st = load().osmx_records_combine(records.data_ptr(), n, k, out_rec.data_ptr(),
+                                     vals.data_ptr() if k > 0 else None, idx.data_ptr() if k > 0 else None,
+                                     ws.data_ptr(), ws.numel(), stream)
+    _raise(st)
+    if check:
+        check_status(ws, stream)
+    return vals[:k], idx[:k], out_rec
+
+
+def scale_with_record(x_slice, record, out=None):
+    """y = e^(x - M)/D over a slice with (M, D) from a merged record."""
+    import torch
+
+    x1 = _check_tensor(x_slice)
+    if out is None:
+        out = torch.empty_like(x1)
+    st = load().osmx_scale_with_record(x1.data_ptr(), x1.shape[1], record.data_ptr(), out.data_ptr(),
+                                       _stream_ptr(x1.device))
+    _raise(st)
+    return out

@@ -1,0 +1,301 @@
+"""GPU parity: every batched entry point of the C-ABI against the oracle
+(our C restatement, itself pinned bit-exactly to the reference in
+test_oracle.py) on the same seeded inputs.
+
+Bars (BASELINE.json north_star): fp32 probabilities within max relative
+error 1e-5 (reference values <= 1e-30 skipped, test_softmax.cpp:30); top-K
+indices bit-exact with ties to the lowest index.  Every kernel family
+(resident / stream / split) is forced in turn.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from tests._util import DISTS, dist, max_rel
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5
+SHAPES = {"auto": 0, "resident": 1, "stream": 2, "split": 3}
+
+
+@pytest.fixture
+def lib():
+    from paper_1805_02867_b200 import _lib
+
+    _lib.load()
+    yield _lib
+    _lib.config_set("shape", 0)
+    _lib.config_set("split_chunk", 0)
+
+
+def _dev(x):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+SOFTMAX_V = [1, 2, 3, 5, 10, 17, 32, 33, 100, 255, 256, 1000, 1023, 1025, 2048, 4099, 8192, 16384, 16387, 70001]
+
+
+@pytest.mark.parametrize("shape", ["auto", "resident", "stream", "split"])
+@pytest.mark.parametrize("alg", ["naive", "safe", "online"])
+def test_softmax_parity(cuda, oracle_mod, lib, alg, shape):
+    from paper_1805_02867_b200 import osmx
+
+    lib.config_set("shape", SHAPES[shape])
+    if shape == "split":
+        lib.config_set("split_chunk", 4096)
+    rng = np.random.default_rng(100 + SHAPES[shape])
+    worst = 0.0
+    for V in SOFTMAX_V:
+        if shape == "resident" and V > 16384:
+            continue
+        for d in DISTS:
+            if alg == "naive" and d in ("wide", "spikes", "quantized100"):
+                continue  # overflow regime: covered by test_naive_overflow
+            rows = 3 if V > 10000 else 7
+            x = dist(d, rng, rows, V)
+            y = osmx.softmax(_dev(x), alg=alg).cpu().numpy()
+            ref, st = oracle_mod.batch(f"{alg}_softmax", x)
+            assert (st == 0).all()
+            err = max_rel(y, ref)
+            worst = max(worst, err)
+            assert err <= TOL, f"{alg}/{shape} V={V} dist={d}: max rel err {err:.3g}"
+    print(f"{alg}/{shape}: worst rel err {worst:.3g}")
+
+
+@pytest.mark.parametrize("alg", ["safe", "online", "naive"])
+def test_softmax_strided_and_misaligned(cuda, oracle_mod, lib, alg):
+    """Leading dimension > V and a row base that is not 16-byte aligned
+    exercise the head/body/tail split of every row."""
+    import torch
+
+    from paper_1805_02867_b200 import osmx
+
+    rng = np.random.default_rng(7)
+    for shape in (0, 2, 3):
+        lib.config_set("shape", shape)
+        lib.config_set("split_chunk", 4096 if shape == 3 else 0)
+        for V in (5, 999, 20001):
+            big = rng.standard_normal((6, V + 7)).astype(np.float32)
+            xt = torch.from_numpy(big).cuda()[:, 1 : V + 1]  # ld = V+7, base offset 4 bytes
+            y = osmx.softmax(xt, alg=alg).cpu().numpy()
+            ref, _ = oracle_mod.batch(f"{alg}_softmax", np.ascontiguousarray(big[:, 1 : V + 1]))
+            assert max_rel(y, ref) <= TOL, (alg, shape, V)
+
+
+def test_softmax_known_answers(cuda, lib):
+    """test_softmax.cpp:37-102 goldens through the device path."""
+    from paper_1805_02867_b200 import osmx
+
+    def sm(a, x):
+        return osmx.softmax(_dev(np.asarray(x, np.float32).reshape(1, -1)), alg=a).cpu().numpy()[0]
+
+    for a in ("naive", "safe", "online"):
+        assert sm(a, [0.0])[0] == 1.0
+        for c in (0.0, 1.5, -20.0, 13.25):
+            assert (sm(a, [c] * 4) == 0.25).all()
+    assert sm("safe", [-123.5])[0] == 1.0
+    assert sm("online", [87.0])[0] == 1.0
+    assert (sm("safe", [2.0] * 5) == np.float32(1.0 / 5.0)).all()
+    yn = sm("naive", [100.0, 100.0])
+    assert np.isnan(yn).all()
+    for a in ("safe", "online"):
+        assert (sm(a, [100.0, 100.0]) == 0.5).all()
+    assert not np.isfinite(sm("naive", [50.0, 89.0, 0.0])).all()
+    assert np.isfinite(sm("safe", [50.0, 89.0, 0.0])).all()
+    k123 = np.array([0.090030573170380462, 0.24472847105479764, 0.66524095577482178])
+    for a in ("naive", "safe", "online"):
+        assert max_rel(sm(a, [1.0, 2.0, 3.0]), k123) <= 1e-6
+    y = sm("safe", [-87.0, 0.0])
+    assert abs(y[0] - 1.6458114537543937e-38) <= 1e-6 * 1.6458114537543937e-38
+    assert y[1] == 1.0
+    yo = sm("online", [-87.0, 0.0])
+    assert yo[0] == y[0] and yo[1] == 1.0
+
+
+def test_naive_overflow_positions(cuda, oracle_mod, lib):
+    """Naive has no overflow guard: non-finite output positions must match the
+    reference's (kernels.hpp:39-46)."""
+    from paper_1805_02867_b200 import osmx
+
+    rng = np.random.default_rng(11)
+    for V in (3, 100, 5000):
+        x = (rng.uniform(80, 200, size=(4, V)) * rng.choice([-1, 1], size=(4, V))).astype(np.float32)
+        y = osmx.softmax(_dev(x), alg="naive").cpu().numpy()
+        ref, _ = oracle_mod.batch("naive_softmax", x)
+        assert np.array_equal(np.isfinite(y), np.isfinite(ref))
+        assert np.array_equal(np.isnan(y), np.isnan(ref))
+        fin = np.isfinite(ref)
+        assert np.allclose(y[fin], ref[fin], rtol=1e-5, atol=1e-30)
+
+
+TOPK_V = [1, 2, 5, 10, 33, 100, 1000, 2049, 4099, 32768, 100003]
+
+
+def _topk_ref(oracle_mod, op, x, k):
+    v, z, st = oracle_mod.batch(op, x, k=k)
+    assert (st == 0).all()
+    return v, z
+
+
+@pytest.mark.parametrize("shape", ["auto", "stream", "split"])
+@pytest.mark.parametrize("k", [1, 2, 5, 8, 13, 32])
+def test_online_fused_topk_parity(cuda, oracle_mod, lib, shape, k):
+    """Alg. 4: indices bit-exact (ties to the lowest index), values 1e-5."""
+    from paper_1805_02867_b200 import osmx
+
+    lib.config_set("shape", SHAPES[shape])
+    if shape == "split":
+        lib.config_set("split_chunk", 2048)
+    rng = np.random.default_rng(200 + k)
+    for V in TOPK_V:
+        if k > V:
+            continue
+        for d in DISTS:
+            rows = 3 if V > 10000 else 9
+            x = dist(d, rng, rows, V)
+            vals, idx = osmx.softmax_topk(_dev(x), k, alg="online_fused")
+            rv, rz = _topk_ref(oracle_mod, "online_softmax_topk", x, k)
+            got = idx.cpu().numpy()
+            assert np.array_equal(got, rz), f"V={V} k={k} {d} {shape}: {got[:2]} vs {rz[:2]}"
+            assert max_rel(vals.cpu().numpy(), rv) <= TOL
+
+
+@pytest.mark.parametrize("shape", ["auto", "split"])
+@pytest.mark.parametrize("k", [1, 5, 16])
+def test_topk_of_parity(cuda, oracle_mod, lib, shape, k):
+    """topk_of: values and indices bit-exact (kernels.hpp:72-83)."""
+    from paper_1805_02867_b200 import osmx
+
+    lib.config_set("shape", SHAPES[shape])
+    if shape == "split":
+        lib.config_set("split_chunk", 2048)
+    rng = np.random.default_rng(300 + k)
+    for V in TOPK_V:
+        if k > V:
+            continue
+        for d in DISTS:
+            x = dist(d, rng, 5, V)
+            vals, idx = osmx.topk(_dev(x), k)
+            rv, rz = _topk_ref(oracle_mod, "topk_of", x, k)
+            assert np.array_equal(idx.cpu().numpy(), rz)
+            assert np.array_equal(vals.cpu().numpy().view(np.int32), rv.view(np.int32))
+
+
+def _prob_collisions(got_idx, ref_idx, ref_probs_row_fn):
+    """Number of rows whose index lists differ; each difference must be a
+    probability-rounding collision (values equal within 2 ulp)."""
+    diff = 0
+    for r in range(got_idx.shape[0]):
+        if not np.array_equal(got_idx[r], ref_idx[r]):
+            p = ref_probs_row_fn(r)
+            a = p[got_idx[r]].astype(np.float64)
+            b = p[ref_idx[r]].astype(np.float64)
+            assert np.allclose(np.sort(a), np.sort(b), rtol=2.5e-7, atol=0), (r, got_idx[r], ref_idx[r])
+            diff += 1
+    return diff
+
+
+@pytest.mark.parametrize("alg,op,base", [
+    ("safe_fused", "safe_softmax_fused_topk", "safe_softmax"),
+    ("safe_unfused", "safe_softmax_then_topk", "safe_softmax"),
+    ("online_unfused", None, "online_softmax"),
+])
+@pytest.mark.parametrize("shape", ["auto", "split"])
+def test_probability_selection_topk(cuda, oracle_mod, lib, alg, op, base, shape):
+    """Selection on probabilities: indices equal to the reference's except
+    where two probabilities collide in fp32 rounding (flagged, counted)."""
+    from paper_1805_02867_b200 import osmx
+
+    lib.config_set("shape", SHAPES[shape])
+    if shape == "split":
+        lib.config_set("split_chunk", 2048)
+    rng = np.random.default_rng(400)
+    collisions = 0
+    for V in TOPK_V:
+        for d in DISTS:
+            k = min(5, V)
+            x = dist(d, rng, 5, V)
+            vals, idx = osmx.softmax_topk(_dev(x), k, alg=alg)
+            y, _ = oracle_mod.batch(base, x)
+            if op is None:
+                rv, rz = _topk_ref(oracle_mod, "topk_of", y, k)
+            else:
+                rv, rz = _topk_ref(oracle_mod, op, x, k)
+            gi = idx.cpu().numpy()
+            collisions += _prob_collisions(gi, rz, lambda r: y[r])
+            assert max_rel(vals.cpu().numpy(), rv) <= TOL
+    print(f"{alg}/{shape}: rows with probability-rounding collisions: {collisions}")
+
+
+def test_topk_known_answers(cuda, lib):
+    """SPEC.md:208-233, 294-295 examples and the signed-zero tie probe."""
+    from paper_1805_02867_b200 import osmx
+
+    def tk(x, k, alg="online_fused"):
+        v, z = osmx.softmax_topk(_dev(np.asarray(x, np.float32).reshape(1, -1)), k, alg=alg)
+        return v.cpu().numpy()[0], z.cpu().numpy()[0]
+
+    def to(x, k):
+        v, z = osmx.topk(_dev(np.asarray(x, np.float32).reshape(1, -1)), k)
+        return v.cpu().numpy()[0], z.cpu().numpy()[0]
+
+    assert list(to([0.1, 0.7, 0.2], 2)[1]) == [1, 2]
+    assert list(to([0.5, 0.5], 1)[1]) == [0]
+    assert list(to([3, 1, 2], 3)[1]) == [0, 2, 1]
+    assert list(to([1, 1, 1], 2)[1]) == [0, 1]
+    for alg in ("online_fused", "safe_fused", "safe_unfused", "online_unfused"):
+        v, z = tk([1, 2, 3], 2, alg)
+        assert list(z) == [2, 1]
+        assert abs(v[0] - 0.66524095577482178) <= 1e-6 and abs(v[1] - 0.24472847105479764) <= 1e-6
+        v, z = tk([5.0], 1, alg)
+        assert list(z) == [0] and v[0] == 1.0
+        assert list(tk([2, 2, 1], 2, alg)[1]) == [0, 1]
+    assert list(tk([0.0, -0.0, 1.0, 1.0, -0.0, 0.0], 4)[1]) == [2, 3, 0, 1]
+
+
+def test_nonfinite_rows_flagged(cuda, lib):
+    """NaN / +inf / -inf anywhere in a row -> non_finite_error naming the first
+    bad row (kernels.hpp:32-35, normalizer.hpp:33)."""
+    from paper_1805_02867_b200 import osmx
+
+    rng = np.random.default_rng(5)
+    for shape in (0, 1, 2, 3):
+        lib.config_set("shape", shape)
+        lib.config_set("split_chunk", 2048 if shape == 3 else 0)
+        for bad in (np.nan, np.inf, -np.inf):
+            for V in (7, 3000, 40000):
+                if shape == 1 and V > 16384:
+                    continue
+                x = rng.standard_normal((6, V)).astype(np.float32)
+                x[4, V // 2] = bad
+                x[5, 0] = bad
+                for alg in ("naive", "safe", "online"):
+                    with pytest.raises(osmx.NonFiniteError) as e:
+                        osmx.softmax(_dev(x), alg=alg)
+                    assert e.value.row == 4, (shape, bad, V, alg)
+                for alg in ("online_fused", "safe_fused", "safe_unfused", "online_unfused"):
+                    with pytest.raises(osmx.NonFiniteError) as e:
+                        osmx.softmax_topk(_dev(x), 3, alg=alg)
+                    assert e.value.row == 4, (shape, bad, V, alg)
+                with pytest.raises(osmx.NonFiniteError):
+                    osmx.topk(_dev(x), 3)
+        # a clean call afterwards succeeds (the flag was cleared)
+        osmx.softmax(_dev(rng.standard_normal((2, 50)).astype(np.float32)))
+
+
+def test_argument_errors(cuda, lib):
+    from paper_1805_02867_b200 import osmx
+
+    x = _dev(np.zeros((2, 4), np.float32))
+    with pytest.raises(osmx.InvalidKError):
+        osmx.softmax_topk(x, 0)
+    with pytest.raises(osmx.InvalidKError):
+        osmx.softmax_topk(x, 5)
+    with pytest.raises(osmx.UnsupportedError):
+        osmx.softmax_topk(_dev(np.zeros((1, 100), np.float32)), 33)
+    with pytest.raises(osmx.EmptyInputError):
+        osmx.softmax(_dev(np.zeros((2, 0), np.float32)))
