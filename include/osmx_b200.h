@@ -157,7 +157,7 @@ uint64_t osmx_launch_count(void);
  *   "resident_max_v" largest V held in registers (<= 16384)
  *   "split_chunk"    elements per CTA in split mode (0 = auto)
  *   "stream_threads" CTA size of the stream kernels (0, 256, 512, 1024)
- *   "topk_threads"   CTA size of the fused top-K (0, 128, 256, 512)
+ *   "topk_threads"   threads per row of the row top-K (0 auto, 32, 128, 256, 512)
  *   "host_chunk_mb"  staging block of the host path (default 512)
  * Returns OSMX_ERR_INVALID_ARG for an unknown key. */
 osmx_status osmx_config_set(const char* key, int64_t value);

@@ -86,6 +86,81 @@ struct MD {
 
 __device__ __forceinline__ MD md_identity() { return MD{kNegInf, 0.0f}; }
 
+// 2^k for an integer-valued k <= 0 (or -inf): exact, by exponent bits.
+__device__ __forceinline__ float pow2_int(float k) {
+  return k < -126.0f ? 0.0f : __int_as_float(((int)k + 127) << 23);
+}
+
+// Per-thread online normalizer in the log2 domain (Alg. 3 lines 1-6 with a
+// cheaper inner step).  d is kept relative to an INTEGER reference
+// n = ceil(m * log2 e), so each term is one FFMA + one ex2:
+//     e_j = 2^(x_j*L - n)        (x_j*L - n is exact before the one rounding)
+// and a rescale when the max grows is an exact power of two.  finish()
+// converts to the reference's (m, d = sum e^(x - m)) with one FFMA whose
+// result lies in [0, 1) -- so |m| never enters a rounding error, unlike
+// ex2(x*L - m*L).  The remaining approximation, L = RN(log2 e), perturbs
+// each term by |x_j - m| * 2^-25, as in e^(x - m) itself.
+//
+// Inputs above 2^127 (m * L would overflow n) switch the thread to `huge`
+// mode for the rest of the row: d relative to m in natural units, terms
+// e^(x - m) as before -- a warp-uniform branch per batch, never taken on
+// ordinary logits.
+constexpr float kHugeX = 1.7014118e38f;  // 2^127
+
+struct L2Acc {
+  float m = kNegInf;  // running max (natural units)
+  float n = kNegInf;  // integer reference, >= m * L up to rounding
+  float d = 0.0f;     // sum 2^(x*L - n)   (huge: sum e^(x - m))
+  bool huge = false;
+
+  // Raise the reference for a batch whose max is bm (no-op if bm <= m).
+  __device__ __forceinline__ void raise(float bm) {
+    if (bm > m) {
+      if (!huge && bm < kHugeX) {
+        const float nn = ceilf(bm * kLog2e);
+        d *= pow2_int(n - nn);
+        n = nn;
+      } else if (!huge) {  // leave the log2 domain: d relative to bm
+        d = (m == kNegInf) ? d : d * ex2(fmaf(-bm, kLog2e, n));
+        huge = isfinite(bm);
+        n = bm;
+        if (!huge) d *= 0.0f;  // +inf input: keep NaN poison, zero otherwise
+      } else {
+        d *= exp_sub(m, bm);
+      }
+      m = bm;
+    }
+  }
+  __device__ __forceinline__ float term(float x) const {
+    return huge ? exp_sub(x, m) : ex2(fmaf(x, kLog2e, -n));
+  }
+  template <int U>
+  __device__ __forceinline__ void add_batch(const float4 (&v)[U]) {
+    float s = 0.0f;
+    if (!huge) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const float a = ex2(fmaf(v[u].x, kLog2e, -n)), b = ex2(fmaf(v[u].y, kLog2e, -n));
+        const float c = ex2(fmaf(v[u].z, kLog2e, -n)), e = ex2(fmaf(v[u].w, kLog2e, -n));
+        s += (a + b) + (c + e);
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        s += (exp_sub(v[u].x, m) + exp_sub(v[u].y, m)) + (exp_sub(v[u].z, m) + exp_sub(v[u].w, m));
+    }
+    d += s;
+  }
+  __device__ __forceinline__ void add1(float x) {
+    raise(x);
+    d += term(x);
+  }
+  __device__ __forceinline__ MD finish() const {
+    if (huge || m == kNegInf || !(m == m)) return MD{m, d};
+    return MD{m, d * ex2(fmaf(-m, kLog2e, n))};
+  }
+};
+
 // merge(), reference normalizer.hpp:52-58.  The identity (-inf, 0) is
 // absorbing without the NaN that (-inf) - (-inf) would produce.
 __device__ __forceinline__ MD md_merge(MD a, MD b) {

@@ -36,6 +36,9 @@ struct Tuning {
   long long split_chunk = 0;    // elements per CTA in split mode (0 = auto)
   int stream_threads = 0;       // CTA size for stream kernels (0 = auto)
   int topk_threads = 0;         // CTA size for the fused top-K (0 = auto)
+  int tma = 0;                  // TMA-ring top-K: 0 off (default: the warp-per-row
+                                // LDG kernel measures faster), 1 auto, 2 force
+  int topk_unroll = 4;          // float4s in flight per thread in the row top-K (4, 8)
 };
 Tuning& tuning();
 

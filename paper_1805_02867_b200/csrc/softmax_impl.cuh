@@ -155,13 +155,15 @@ __global__ void __launch_bounds__(TPR > 256 ? TPR : 256)
     float lm = kNegInf;
 #pragma unroll
     for (int t = 0; t < EPT; ++t) lm = fmaxf(lm, a[t]);
-    float ld = 0.0f;
+    L2Acc acc;
+    acc.raise(lm);
     if (lm != kNegInf) {
 #pragma unroll
-      for (int t = 0; t < EPT; ++t) ld += exp_sub(a[t], lm);
+      for (int t = 0; t < EPT; ++t) acc.d += acc.term(a[t]);
     }
-    if (bad) ld = nanf_();
-    MD s = G::md(MD{lm, ld}, smf);
+    MD s0 = acc.finish();
+    if (bad) s0.d = nanf_();
+    MD s = G::md(s0, smf);
     m = s.m;
     r = __frcp_rn(s.d);
     row_bad = !(s.d == s.d) || !isfinite(m);
@@ -170,9 +172,11 @@ __global__ void __launch_bounds__(TPR > 256 ? TPR : 256)
 #pragma unroll
     for (int t = 0; t < EPT; ++t) lm = fmaxf(lm, a[t]);
     m = G::reduce(lm, OpMax(), smf);
-    float ld = 0.0f;
+    L2Acc acc;
+    acc.raise(m);
 #pragma unroll
-    for (int t = 0; t < EPT; ++t) ld += exp_sub(a[t], m);
+    for (int t = 0; t < EPT; ++t) acc.d += acc.term(a[t]);
+    float ld = (m == kNegInf) ? 0.0f : acc.finish().d;
     if (bad) ld = nanf_();
     const float d = G::reduce(ld, OpSum(), smf);
     r = __frcp_rn(d);
@@ -231,17 +235,12 @@ __global__ void __launch_bounds__(BLOCK)
     bool bad;
     if constexpr (ALG == osmx_host::kOnline) {
       // Pass 1: Alg. 3 lines 1-6, batch-max-first update per U float4s.
-      float m = kNegInf, d = 0.0f;
+      L2Acc acc;
       stream_seg<BLOCK, U, false>(
           s, t,
           [&](float v, long long) {
             mn = fminf(mn, v);
-            if (v > m) {
-              d = d * exp_sub(m, v) + 1.0f;
-              m = v;
-            } else {
-              d += exp_sub(v, m);
-            }
+            acc.add1(v);
           },
           [&](float4 (&v)[U], long long, int cnt) {
             float bm = kNegInf, bn = -kNegInf;
@@ -251,17 +250,10 @@ __global__ void __launch_bounds__(BLOCK)
               if (u < cnt) bn = fminf(bn, fminf(fminf(v[u].x, v[u].y), fminf(v[u].z, v[u].w)));
             }
             mn = fminf(mn, bn);
-            if (bm > m) {
-              d *= exp_sub(m, bm);
-              m = bm;
-            }
-            float sum = 0.0f;
-#pragma unroll
-            for (int u = 0; u < U; ++u)
-              sum += (exp_sub(v[u].x, m) + exp_sub(v[u].y, m)) + (exp_sub(v[u].z, m) + exp_sub(v[u].w, m));
-            d += sum;
+            acc.raise(bm);
+            acc.add_batch<U>(v);
           });
-      MD tot = md_cta_reduce<NW>(MD{m, d}, smf);
+      MD tot = md_cta_reduce<NW>(acc.finish(), smf);
       mn = cta_min<NW>(mn, smf);
       M = tot.m;
       r = __frcp_rn(tot.d);
@@ -285,16 +277,12 @@ __global__ void __launch_bounds__(BLOCK)
           });
       M = cta_max<NW>(m, smf);
       mn = cta_min<NW>(mn, smf);
-      float d = 0.0f;
+      L2Acc sacc;  // sum e^(x - M) as one FFMA + ex2 per element
+      sacc.raise(M);
       stream_seg<BLOCK, U, false>(
-          s, t, [&](float v, long long) { d += exp_sub(v, M); },
-          [&](float4 (&v)[U], long long, int) {
-            float sum = 0.0f;
-#pragma unroll
-            for (int u = 0; u < U; ++u)
-              sum += (exp_sub(v[u].x, M) + exp_sub(v[u].y, M)) + (exp_sub(v[u].z, M) + exp_sub(v[u].w, M));
-            d += sum;
-          });
+          s, t, [&](float v, long long) { sacc.d += sacc.term(v); },
+          [&](float4 (&v)[U], long long, int) { sacc.add_batch<U>(v); });
+      float d = (M == kNegInf) ? 0.0f : sacc.finish().d;
       d = cta_sum<NW>(d, smf);
       r = __frcp_rn(d);
       bad = !(d == d) || !isfinite(M) || mn == kNegInf;
@@ -368,16 +356,12 @@ __global__ void __launch_bounds__(BLOCK)
     float M = kNegInf;
     for (int i = t; i < S; i += BLOCK) M = fmaxf(M, rr[i].m);
     M = cta_max<NW>(M, smf);
-    float d = 0.0f;
+    L2Acc sacc;  // sum e^(x - M) as one FFMA + ex2 per element
+    sacc.raise(M);
     stream_seg<BLOCK, U, false>(
-        s, t, [&](float v, long long) { d += exp_sub(v, M); },
-        [&](float4 (&v)[U], long long, int) {
-          float sum = 0.0f;
-#pragma unroll
-          for (int u = 0; u < U; ++u)
-            sum += (exp_sub(v[u].x, M) + exp_sub(v[u].y, M)) + (exp_sub(v[u].z, M) + exp_sub(v[u].w, M));
-          d += sum;
-        });
+        s, t, [&](float v, long long) { sacc.d += sacc.term(v); },
+        [&](float4 (&v)[U], long long, int) { sacc.add_batch<U>(v); });
+    float d = (M == kNegInf) ? 0.0f : sacc.finish().d;
     d = cta_sum<NW>(d, smf);
     __syncthreads();  // every thread has read rr[*].m before it is rewritten
     if (t == 0) rr[blockIdx.x].d = (double)d;
@@ -385,17 +369,12 @@ __global__ void __launch_bounds__(BLOCK)
   }
   float mn = -kNegInf;
   if constexpr (ALG == osmx_host::kOnline) {
-    float m = kNegInf, d = 0.0f;
+    L2Acc acc;
     stream_seg<BLOCK, U, false>(
         s, t,
         [&](float v, long long) {
           mn = fminf(mn, v);
-          if (v > m) {
-            d = d * exp_sub(m, v) + 1.0f;
-            m = v;
-          } else {
-            d += exp_sub(v, m);
-          }
+          acc.add1(v);
         },
         [&](float4 (&v)[U], long long, int cnt) {
           float bm = kNegInf, bn = -kNegInf;
@@ -405,17 +384,10 @@ __global__ void __launch_bounds__(BLOCK)
             if (u < cnt) bn = fminf(bn, fminf(fminf(v[u].x, v[u].y), fminf(v[u].z, v[u].w)));
           }
           mn = fminf(mn, bn);
-          if (bm > m) {
-            d *= exp_sub(m, bm);
-            m = bm;
-          }
-          float sum = 0.0f;
-#pragma unroll
-          for (int u = 0; u < U; ++u)
-            sum += (exp_sub(v[u].x, m) + exp_sub(v[u].y, m)) + (exp_sub(v[u].z, m) + exp_sub(v[u].w, m));
-          d += sum;
+          acc.raise(bm);
+          acc.add_batch<U>(v);
         });
-    MD tot = md_cta_reduce<NW>(MD{m, d}, smf);
+    MD tot = md_cta_reduce<NW>(acc.finish(), smf);
     mn = cta_min<NW>(mn, smf);
     if (t == 0) rr[blockIdx.x] = SRec{tot.m, mn, (double)tot.d};
   } else if constexpr (ALG == osmx_host::kSafe) {
@@ -542,17 +514,13 @@ __global__ void __launch_bounds__(BLOCK)
   const int t = threadIdx.x;
   for (long long row = blockIdx.x; row < rows; row += gridDim.x) {
     const Seg s = make_seg(x + row * ldx, V);
-    float m = kNegInf, d = 0.0f, mn = -kNegInf;
+    L2Acc acc;
+    float mn = -kNegInf;
     stream_seg<BLOCK, U, false>(
         s, t,
         [&](float v, long long) {
           mn = fminf(mn, v);
-          if (v > m) {
-            d = d * exp_sub(m, v) + 1.0f;
-            m = v;
-          } else {
-            d += exp_sub(v, m);
-          }
+          acc.add1(v);
         },
         [&](float4 (&v)[U], long long, int cnt) {
           float bm = kNegInf, bn = -kNegInf;
@@ -562,17 +530,10 @@ __global__ void __launch_bounds__(BLOCK)
             if (u < cnt) bn = fminf(bn, fminf(fminf(v[u].x, v[u].y), fminf(v[u].z, v[u].w)));
           }
           mn = fminf(mn, bn);
-          if (bm > m) {
-            d *= exp_sub(m, bm);
-            m = bm;
-          }
-          float sum = 0.0f;
-#pragma unroll
-          for (int u = 0; u < U; ++u)
-            sum += (exp_sub(v[u].x, m) + exp_sub(v[u].y, m)) + (exp_sub(v[u].z, m) + exp_sub(v[u].w, m));
-          d += sum;
+          acc.raise(bm);
+          acc.add_batch<U>(v);
         });
-    MD tot = md_cta_reduce<NW>(MD{m, d}, smf);
+    MD tot = md_cta_reduce<NW>(acc.finish(), smf);
     mn = cta_min<NW>(mn, smf);
     if (t == 0) {
       om[row] = tot.m;

@@ -24,9 +24,21 @@ size_t topk_split_ws(int alg, long long rows, long long V, int k) {
 }
 bool topk_split(long long rows, long long V) { return topk_uses_split(rows, V); }
 
+cudaError_t launch_topk_tma(int mode, const float* x, long long ldx, long long rows, long long V, int k,
+                            float* vals, long long* idx, void* ws, cudaStream_t st);
+
+bool topk_uses_tma(int mode, long long rows, long long V) {
+  const auto& tn = tuning();
+  if (mode == kModeSafe || tn.tma == 0) return false;
+  if (tn.shape == kShapeSplit || tn.shape == kShapeResident) return false;
+  if (tn.tma == 2) return true;
+  return V >= 8192 && rows >= num_sms() && !topk_uses_split(rows, V);
+}
+
 cudaError_t launch_topk_mode(int mode, const float* x, long long ldx, long long rows, long long V, int k,
                              float* vals, long long* idx, void* ws, cudaStream_t st) {
   const bool split = topk_uses_split(rows, V);
+  if (topk_uses_tma(mode, rows, V)) return launch_topk_tma(mode, x, ldx, rows, V, k, vals, idx, ws, st);
   switch (mode) {
     case kModeFused: return launch_topk_fused(x, ldx, rows, V, k, vals, idx, ws, st, split, 0, nullptr);
     case kModeTopkOf: return launch_topk_of(x, ldx, rows, V, k, vals, idx, ws, st, split);

@@ -49,18 +49,14 @@ __host__ __device__ inline size_t rec_bytes_(int k) { return ((rec_idx_off(k) + 
 template <int KC, int U, int MODE, int G>
 struct Pass {
   TopList<KC> L;
-  float m = kNegInf, d = 0.0f, mn = -kNegInf, chk = 0.0f;
+  L2Acc acc;  // online (m, d) of the fused mode
+  float mn = -kNegInf, chk = 0.0f;
   float M = 0.0f, R = 0.0f;  // SAFE select pass: row max and 1/d
 
   __device__ __forceinline__ void scalar(float v, int j, int k) {
     if constexpr (MODE == kModeFused) {
       mn = fminf(mn, v);
-      if (v > m) {
-        d = d * exp_sub(m, v) + 1.0f;
-        m = v;
-      } else {
-        d += exp_sub(v, m);
-      }
+      acc.add1(v);
       L.offer(v, j);
     } else if constexpr (MODE == kModeTopkOf) {
       chk = fmaf(v, 0.0f, chk);  // NaN iff some element was inf / NaN
@@ -70,6 +66,66 @@ struct Pass {
     }
   }
   __device__ __forceinline__ void batch(const Seg& s, float4 (&v)[U], long long q0, int cnt, int k) {
+    batch_j(v, cnt, (int)body_index(s, q0, 0), 4 * G);
+  }
+  // Warp-shared admission bound: the max over (converged) lanes of their own
+  // k-th best.  Every lane's k-th best is <= the row's k-th best, so an
+  // element below T can never be selected; elements equal to T are kept
+  // (index ties).  It keeps warps out of the insertion path after the first
+  // few batches -- without it one inserting lane drags the whole warp in.
+  float T = kNegInf;
+  int* Tsh = nullptr;    // CTA-shared bound (ordered-int float) when the CTA owns one row
+  float best = kNegInf;  // the lane's best key so far
+  int kk = 1;            // runtime k (set by the kernel)
+
+  __device__ __forceinline__ static int f2o(float f) {
+    const int i = __float_as_int(f);
+    return i ^ ((i >> 31) & 0x7fffffff);
+  }
+  __device__ __forceinline__ static float o2f(int i) { return __int_as_float(i ^ ((i >> 31) & 0x7fffffff)); }
+
+  template <class KeyF>
+  __device__ __forceinline__ void select_batch(float4 (&v)[U], int cnt, int j0, int jstride, float bkey,
+                                               KeyF&& key) {
+    const unsigned mask = __activemask();
+    best = fmaxf(best, bkey);
+    bool want = bkey > L.thr() && bkey >= T;
+    if (Tsh && __any_sync(mask, want)) {
+      T = fmaxf(T, o2f(*reinterpret_cast<volatile int*>(Tsh)));  // other warps' progress
+      want = bkey > L.thr() && bkey >= T;
+    }
+    if (__any_sync(mask, want)) {
+      if (want) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (u >= cnt) break;  // padding of the last batch is never offered
+          const int j = j0 + u * jstride;
+          const float k0 = key(v[u].x), k1 = key(v[u].y), k2 = key(v[u].z), k3 = key(v[u].w);
+          if (k0 >= T) L.offer(k0, j);
+          if (k1 >= T) L.offer(k1, j + 1);
+          if (k2 >= T) L.offer(k2, j + 2);
+          if (k3 >= T) L.offer(k3, j + 3);
+        }
+      }
+      // Two valid lower bounds of the row's k-th best: the best lane k-th,
+      // and the k-th largest of the lanes' bests (k distinct elements >= it).
+      int t = __reduce_max_sync(mask, f2o(L.thr()));
+      if (__popc(mask) >= kk) {
+        int mine = f2o(best), kth = mine;
+        for (int r = 0; r < kk; ++r) {
+          kth = __reduce_max_sync(mask, mine);
+          const unsigned who = __ballot_sync(mask, mine == kth);
+          if ((int)(threadIdx.x & 31) == __ffs(who) - 1) mine = f2o(kNegInf);
+        }
+        t = max(t, kth);
+      }
+      T = fmaxf(T, o2f(t));
+      if (Tsh && (int)(threadIdx.x & 31) == __ffs(mask) - 1) atomicMax(Tsh, f2o(T));
+    }
+  }
+
+  // v[u] holds elements j0 + u*jstride + {0,1,2,3} (u < cnt valid).
+  __device__ __forceinline__ void batch_j(float4 (&v)[U], int cnt, int j0, int jstride) {
     if constexpr (MODE == kModeFused) {
       float bm = kNegInf, bn = -kNegInf;
 #pragma unroll
@@ -77,27 +133,12 @@ struct Pass {
         bm = fmaxf(bm, fmaxf(fmaxf(v[u].x, v[u].y), fmaxf(v[u].z, v[u].w)));
         if (u < cnt) bn = fminf(bn, fminf(fminf(v[u].x, v[u].y), fminf(v[u].z, v[u].w)));
       }
-      mn = fminf(mn, bn);
-      if (bm > m) {
-        d *= exp_sub(m, bm);
-        m = bm;
+      if (cnt > 0) {  // an empty batch (TMA tail) must not touch (m, d): e^(-inf - -inf)
+        mn = fminf(mn, bn);
+        acc.raise(bm);
+        acc.add_batch<U>(v);
       }
-      float sum = 0.0f;
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        sum += (exp_sub(v[u].x, m) + exp_sub(v[u].y, m)) + (exp_sub(v[u].z, m) + exp_sub(v[u].w, m));
-      d += sum;
-      if (bm > L.thr()) {
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          if (u >= cnt) break;  // padding of the last batch is never offered
-          const int j = (int)body_index(s, q0 + (long long)u * G, 0);
-          L.offer(v[u].x, j);
-          L.offer(v[u].y, j + 1);
-          L.offer(v[u].z, j + 2);
-          L.offer(v[u].w, j + 3);
-        }
-      }
+      select_batch(v, cnt, j0, jstride, bm, [](float e) { return e; });
     } else if constexpr (MODE == kModeTopkOf) {
       float bm = kNegInf;
 #pragma unroll
@@ -110,33 +151,14 @@ struct Pass {
           chk = fmaf(v[u].w, 0.0f, chk);
         }
       }
-      if (bm > L.thr()) {
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          if (u >= cnt) break;  // padding of the last batch is never offered
-          const int j = (int)body_index(s, q0 + (long long)u * G, 0);
-          L.offer(v[u].x, j);
-          L.offer(v[u].y, j + 1);
-          L.offer(v[u].z, j + 2);
-          L.offer(v[u].w, j + 3);
-        }
-      }
+      select_batch(v, cnt, j0, jstride, bm, [](float e) { return e; });
     } else {
-      // p is monotone in x for a fixed row (M, R): filter on x first.
+      // p is monotone in x for a fixed row (M, R): filter on the batch max.
       float bm = kNegInf;
 #pragma unroll
       for (int u = 0; u < U; ++u) bm = fmaxf(bm, fmaxf(fmaxf(v[u].x, v[u].y), fmaxf(v[u].z, v[u].w)));
-      if (expf(bm - M) * R >= L.thr()) {
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          if (u >= cnt) break;  // padding of the last batch is never offered
-          const int j = (int)body_index(s, q0 + (long long)u * G, 0);
-          L.offer(expf(v[u].x - M) * R, j);
-          L.offer(expf(v[u].y - M) * R, j + 1);
-          L.offer(expf(v[u].z - M) * R, j + 2);
-          L.offer(expf(v[u].w - M) * R, j + 3);
-        }
-      }
+      const float Mr = M, Rr = R;
+      select_batch(v, cnt, j0, jstride, expf(bm - Mr) * Rr, [Mr, Rr](float e) { return expf(e - Mr) * Rr; });
     }
   }
 };
@@ -213,8 +235,8 @@ __device__ __forceinline__ void cta_merge(TopList<KC>& L, int k, float* sv, int*
 // ---------------------------------------------------------- row kernel --
 // G threads per row (G == 32: warp per row, BLOCK/32 rows per CTA; G ==
 // BLOCK: CTA per row).  Rows are visited grid-stride.
-template <int G, int BLOCK, int KC, int MODE, int U>
-__global__ void __launch_bounds__(BLOCK)
+template <int G, int BLOCK, int KC, int MODE, int U, int MINB = 1>
+__global__ void __launch_bounds__(BLOCK, MINB)
     k_topk_rows(const float* __restrict__ x, long long ldx, long long rows, long long V, int k,
                 float* __restrict__ vals, long long* __restrict__ idx, void* ws) {
   constexpr int NW = BLOCK / 32;
@@ -222,14 +244,23 @@ __global__ void __launch_bounds__(BLOCK)
   __shared__ float smf[2 * NW];
   __shared__ float sv[NW * KC];
   __shared__ int si[NW * KC];
+  __shared__ int tsh[2];  // CTA-shared admission bound, double-buffered by row parity
   const int t = threadIdx.x % G;
   const long long nrow_groups = (rows + RPC - 1) / RPC;
-  for (long long rg = blockIdx.x; rg < nrow_groups; rg += gridDim.x) {
+  if (threadIdx.x == 0) tsh[0] = tsh[1] = Pass<KC, U, MODE, G>::f2o(kNegInf);
+  __syncthreads();
+  int it = 0;
+  for (long long rg = blockIdx.x; rg < nrow_groups; rg += gridDim.x, ++it) {
+    // slot it&1 serves this row; the other slot is reset for the next row
+    // (every thread passed the previous row's final barrier before this).
+    if (G == BLOCK && threadIdx.x == 0) tsh[(it + 1) & 1] = Pass<KC, U, MODE, G>::f2o(kNegInf);
     const long long row = rg * RPC + threadIdx.x / G;
     const bool live = row < rows;
     const Seg s = make_seg(x + (live ? row : 0) * ldx, live ? V : 0);
     Pass<KC, U, MODE, G> P;
     P.L.init(k);
+    P.kk = k;
+    if (G == BLOCK) P.Tsh = &tsh[it & 1];
     bool bad = false;
     float outM = 0.0f, outR = 1.0f;
     if constexpr (MODE == kModeSafe) {
@@ -257,10 +288,10 @@ __global__ void __launch_bounds__(BLOCK)
       MD tot;
       float MN;
       if constexpr (G == 32) {
-        tot = md_group_reduce<32>(MD{P.m, P.d});
+        tot = md_group_reduce<32>(P.acc.finish());
         MN = group_min<32>(P.mn);
       } else {
-        tot = md_cta_reduce<NW>(MD{P.m, P.d}, smf);
+        tot = md_cta_reduce<NW>(P.acc.finish(), smf);
         MN = cta_min<NW>(P.mn, smf);
       }
       outM = tot.m;
@@ -315,8 +346,13 @@ __global__ void __launch_bounds__(BLOCK)
   const long long n = std::min(chunk, V - c0);
   const Seg s = make_seg(x + row * ldx + c0, n);
   const int t = threadIdx.x;
+  __shared__ int tsh;
+  if (t == 0) tsh = Pass<KC, U, MODE, BLOCK>::f2o(kNegInf);
+  __syncthreads();
   Pass<KC, U, MODE, BLOCK> P;
   P.L.init(k);
+  P.kk = k;
+  P.Tsh = &tsh;
   float safe_mn = 0.0f;
   if constexpr (MODE == kModeSafe) {
     const SRecView* rr = srec + row * S;
@@ -338,7 +374,7 @@ __global__ void __launch_bounds__(BLOCK)
   run_pass<BLOCK, U, KC, MODE>(P, s, t, k);
   RecHdr h{0.0f, 0.0f, 0.0f, k};
   if constexpr (MODE == kModeFused) {
-    MD tot = md_cta_reduce<NW>(MD{P.m, P.d}, smf);
+    MD tot = md_cta_reduce<NW>(P.acc.finish(), smf);
     h.m = tot.m;
     h.d = tot.d;
     h.mn = cta_min<NW>(P.mn, smf);
@@ -422,20 +458,41 @@ __global__ void __launch_bounds__(32)
 
 // ------------------------------------------------------------ launchers --
 
+// Threads per row: enough rows in flight to fill every SM several times,
+// as few threads per row as that allows (the per-row epilogue -- (m,d)
+// reduce and k-round merge -- is paid once per row, and small CTAs let
+// other CTAs on the SM keep streaming while one merges).
+inline int topk_row_threads(long long rows, long long V) {
+  const int forced = osmx_host::tuning().topk_threads;
+  if (forced) return forced;
+  const long long sms = osmx_host::num_sms();
+  // measured on B200 (profiles/): warp-per-row reads C4 at 7.1 TB/s vs 6.5
+  // (128 threads) and 5.9 (256); it wins down to ~4000 rows.
+  if (V <= 2048 || rows >= 16 * sms) return 32;
+  if (rows >= 4 * sms) return 128;
+  return 256;
+}
+
 template <int KC, int MODE>
 cudaError_t run_rows(const float* x, long long ldx, long long rows, long long V, int k, float* vals,
                      long long* idx, void* ws, cudaStream_t st) {
-  const int sms = osmx_host::num_sms();
-  int threads = osmx_host::tuning().topk_threads;
-  if (V <= 2048 && threads == 0) {
+  const int g = topk_row_threads(rows, V);
+  if (g == 32) {
     constexpr int RPC = 256 / 32;
     const long long groups = (rows + RPC - 1) / RPC;
     const long long grid = std::min<long long>(groups, 1LL << 30);
-    k_topk_rows<32, 256, KC, MODE, 2><<<(unsigned)grid, 256, 0, st>>>(x, ldx, rows, V, k, vals, idx, ws);
+    if (V <= 2048)
+      k_topk_rows<32, 256, KC, MODE, 2, 4><<<(unsigned)grid, 256, 0, st>>>(x, ldx, rows, V, k, vals, idx, ws);
+    else
+      k_topk_rows<32, 256, KC, MODE, 4, 4><<<(unsigned)grid, 256, 0, st>>>(x, ldx, rows, V, k, vals, idx, ws);
   } else {
-    (void)sms;
     const long long grid = std::min<long long>(rows, 1LL << 30);
-    k_topk_rows<256, 256, KC, MODE, 4><<<(unsigned)grid, 256, 0, st>>>(x, ldx, rows, V, k, vals, idx, ws);
+    if (g == 128)
+      k_topk_rows<128, 128, KC, MODE, 4, 8><<<(unsigned)grid, 128, 0, st>>>(x, ldx, rows, V, k, vals, idx, ws);
+    else if (g == 512)
+      k_topk_rows<512, 512, KC, MODE, 4, 2><<<(unsigned)grid, 512, 0, st>>>(x, ldx, rows, V, k, vals, idx, ws);
+    else
+      k_topk_rows<256, 256, KC, MODE, 4, 4><<<(unsigned)grid, 256, 0, st>>>(x, ldx, rows, V, k, vals, idx, ws);
   }
   osmx_host::count_launch();
   return cudaGetLastError();

@@ -1,0 +1,251 @@
+// topk_tma.cu -- persistent, TMA-fed fused online softmax + top-K
+// (Alg. 4, reference online_softmax_topk_kernel kernels.hpp:108-125) and
+// topk_of (kernels.hpp:72-83) for many rows of large V.
+//
+// Structure (one CTA per SM slot, rows visited grid-stride):
+//   warp NCW      producer: lane 0 streams every row's 16-byte aligned body
+//                 through a STAGES x CHUNK shared-memory ring with 1-D bulk
+//                 copies (cp.async.bulk, evict-first), one mbarrier pair per
+//                 stage.  It runs ahead across row boundaries, so the next
+//                 row is already in flight while consumers merge this one.
+//   warps 0..NCW-1 consumers: per stage, each thread takes U float4s
+//                 (LDS.128), updates its online (m, d) with a batch-max-first
+//                 rescale and offers batch survivors to its register top-K
+//                 list; at row end a named-barrier CTA reduce (Eq. 4 merge)
+//                 and a k-round list merge under (value desc, index asc).
+// Head / tail elements outside the aligned body (V % 4 or unaligned rows)
+// are read directly from global memory by the first consumer threads, first
+// and last respectively, so every thread still sees its elements in
+// increasing index order (the reference's tie rule, topk.hpp:37-43).
+#include "topk_impl.cuh"
+#include "tma.cuh"
+
+namespace {
+
+constexpr int kChunk = 16384;  // bytes per stage (4096 floats)
+
+// Consumer-group reductions over NC threads using named barrier 1.
+template <int NCW>
+__device__ __forceinline__ MD md_group_cta(MD s, float* sm) {
+  s = md_group_reduce<32>(s);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) {
+    sm[w] = s.m;
+    sm[NCW + w] = s.d;
+  }
+  named_sync(1, NCW * 32);
+  MD t = md_identity();
+  if (l < NCW) t = MD{sm[l], sm[NCW + l]};
+  t = md_group_reduce<32>(t);
+  named_sync(1, NCW * 32);
+  return t;
+}
+template <int NCW, class Op>
+__device__ __forceinline__ float red_group_cta(float v, float init, Op op, float* sm) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) sm[w] = v;
+  named_sync(1, NCW * 32);
+  float t = l < NCW ? sm[l] : init;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t = op(t, __shfl_xor_sync(0xffffffffu, t, o));
+  named_sync(1, NCW * 32);
+  return t;
+}
+
+template <int NCW, int KC, class Sink>
+__device__ __forceinline__ void merge_group_cta(TopList<KC>& L, int k, float* sv, int* si, Sink&& sink) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  L.normalize(k);
+  group_merge<32>(L, k, [&](int r, float v, int i) {
+    if (l == 0) {
+      sv[w * KC + r] = v;
+      si[w * KC + r] = i;
+    }
+  });
+  named_sync(1, NCW * 32);
+  if (w == 0) {
+    TopList<KC> M;
+    M.init_empty();
+    if (l < NCW) {
+#pragma unroll
+      for (int r = 0; r < KC; ++r)
+        if (r < k) {
+          M.v[r] = sv[l * KC + r];
+          M.i[r] = si[l * KC + r];
+        }
+    }
+    group_merge<32>(M, k, sink);
+  }
+  named_sync(1, NCW * 32);
+}
+
+struct MinOp {
+  __device__ float operator()(float a, float b) const { return fminf(a, b); }
+};
+struct SumOp {
+  __device__ float operator()(float a, float b) const { return a + b; }
+};
+
+template <int NCW, int STAGES, int KC, int MODE>
+__global__ void __launch_bounds__((NCW + 1) * 32)
+    k_topk_tma(const float* __restrict__ x, long long ldx, long long rows, long long V, int k,
+               float* __restrict__ vals, long long* __restrict__ idx, void* ws) {
+  constexpr int NC = NCW * 32;
+  constexpr int U = kChunk / 16 / NC;  // float4s per consumer thread per stage
+  static_assert(U >= 1 && U * NC * 16 == kChunk, "chunk must split evenly");
+  extern __shared__ __align__(128) unsigned char smem[];
+  float4* ring = reinterpret_cast<float4*>(smem);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * kChunk);
+  uint64_t* empty = full + STAGES;
+  float* smf = reinterpret_cast<float*>(empty + STAGES);  // 2*NCW
+  float* sv = smf + 2 * NCW;                              // NCW*KC
+  int* si = reinterpret_cast<int*>(sv + NCW * KC);        // NCW*KC
+  int* tsh = si + NCW * KC;                               // 2 (row parity)
+
+  const int w = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NCW);
+    }
+    fence_mbar_init();
+    tsh[0] = tsh[1] = Pass<KC, 1, MODE, NCW * 32>::f2o(kNegInf);
+  }
+  __syncthreads();
+
+  if (w == NCW) {
+    // ------------------------------------------------------- producer
+    if ((threadIdx.x & 31) == 0) {
+      const uint64_t pol = pol_evict_first();
+      int s = 0;
+      uint32_t ph = 0;
+      for (long long row = blockIdx.x; row < rows; row += gridDim.x) {
+        const Seg sg = make_seg(x + row * ldx, V);
+        const char* b = reinterpret_cast<const char*>(sg.p + sg.head);
+        const long long bytes = sg.nvec * 16;
+        for (long long off = 0; off < bytes; off += kChunk) {
+          const uint32_t n = (uint32_t)(bytes - off < kChunk ? bytes - off : kChunk);
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_arrive_expect_tx(&full[s], n);
+          tma_load_1d(reinterpret_cast<char*>(ring) + (size_t)s * kChunk, b + off, n, &full[s], pol);
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // --------------------------------------------------------- consumers
+  const int t = threadIdx.x;
+  int s = 0;
+  uint32_t ph = 0;
+  int it = 0;
+  for (long long row = blockIdx.x; row < rows; row += gridDim.x, ++it) {
+    const Seg sg = make_seg(x + row * ldx, V);
+    if (t == 0) tsh[(it + 1) & 1] = Pass<KC, U, MODE, NC>::f2o(kNegInf);
+    Pass<KC, U, MODE, NC> P;
+    P.L.init(k);
+    P.kk = k;
+    P.Tsh = &tsh[it & 1];
+    if (t < sg.head) P.scalar(ld_f1(sg.p + t), t, k);
+    const long long bytes = sg.nvec * 16;
+    for (long long off = 0; off < bytes; off += kChunk) {
+      const int n4 = (int)((bytes - off < kChunk ? bytes - off : kChunk) >> 4);
+      mbar_wait(&full[s], ph);
+      const float4* sb = ring + (size_t)s * (kChunk / 16);
+      float4 v[U];
+      int cnt = 0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int q = t + u * NC;
+        if (q < n4) {
+          v[u] = sb[q];
+          cnt = u + 1;
+        } else {
+          v[u] = make_float4(kNegInf, kNegInf, kNegInf, kNegInf);
+        }
+      }
+      __syncwarp();
+      if ((t & 31) == 0) mbar_arrive(&empty[s]);
+      if (++s == STAGES) {
+        s = 0;
+        ph ^= 1;
+      }
+      P.batch_j(v, cnt, sg.head + (int)(off >> 2) + 4 * t, 4 * NC);  // warp-uniform call
+    }
+    if (t < sg.tail) {
+      const int j = sg.head + (int)(4 * sg.nvec) + t;
+      P.scalar(ld_f1(sg.p + j), j, k);
+    }
+    // ---- row epilogue (consumers only)
+    float outM = 0.0f, outR = 1.0f;
+    bool bad;
+    if constexpr (MODE == kModeFused) {
+      const MD tot = md_group_cta<NCW>(P.acc.finish(), smf);
+      const float mn = red_group_cta<NCW>(P.mn, -kNegInf, MinOp(), smf);
+      outM = tot.m;
+      outR = __frcp_rn(tot.d);
+      bad = !(tot.d == tot.d) || !isfinite(tot.m) || mn == kNegInf;
+    } else {
+      const float c = red_group_cta<NCW>(P.chk, 0.0f, SumOp(), smf);
+      bad = !(c == c);
+    }
+    merge_group_cta<NCW>(P.L, k, sv, si, [&](int r, float v, int i) {
+      if ((int)(threadIdx.x & 31) == (r & 31)) {
+        float out = v;
+        if constexpr (MODE == kModeFused) out = expf(v - outM) * outR;  // kernels.hpp:122
+        vals[row * k + r] = out;
+        idx[row * k + r] = (long long)i;
+      }
+    });
+    if (bad && t == 0) flag_bad_row(ws, row);
+  }
+}
+
+constexpr int kNCW = 8;
+constexpr int kStages = 3;
+
+template <int KC, int MODE>
+cudaError_t run_tma(const float* x, long long ldx, long long rows, long long V, int k, float* vals,
+                    long long* idx, void* ws, cudaStream_t st) {
+  auto kern = k_topk_tma<kNCW, kStages, KC, MODE>;
+  const size_t smem = (size_t)kStages * kChunk + 2 * kStages * sizeof(uint64_t) + 2 * kNCW * sizeof(float) +
+                      (size_t)kNCW * KC * (sizeof(float) + sizeof(int)) + 2 * sizeof(int);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  static int per_sm = 0;  // per instantiation (same on every sm_100 device)
+  if (per_sm == 0) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (kNCW + 1) * 32, smem);
+    if (per_sm < 1) per_sm = 1;
+  }
+  const long long grid = std::min<long long>(rows, (long long)per_sm * osmx_host::num_sms());
+  kern<<<(unsigned)grid, (kNCW + 1) * 32, smem, st>>>(x, ldx, rows, V, k, vals, idx, ws);
+  osmx_host::count_launch();
+  return cudaGetLastError();
+}
+
+template <int MODE>
+cudaError_t dispatch_tma(const float* x, long long ldx, long long rows, long long V, int k, float* vals,
+                         long long* idx, void* ws, cudaStream_t st) {
+  if (k <= 1) return run_tma<1, MODE>(x, ldx, rows, V, k, vals, idx, ws, st);
+  if (k <= 5) return run_tma<5, MODE>(x, ldx, rows, V, k, vals, idx, ws, st);
+  if (k <= 8) return run_tma<8, MODE>(x, ldx, rows, V, k, vals, idx, ws, st);
+  if (k <= 16) return run_tma<16, MODE>(x, ldx, rows, V, k, vals, idx, ws, st);
+  return run_tma<32, MODE>(x, ldx, rows, V, k, vals, idx, ws, st);
+}
+
+}  // namespace
+
+namespace osmx_host {
+// mode 0: fused online softmax + top-K; mode 1: topk_of.
+cudaError_t launch_topk_tma(int mode, const float* x, long long ldx, long long rows, long long V, int k,
+                            float* vals, long long* idx, void* ws, cudaStream_t st) {
+  if (mode == kModeFused) return dispatch_tma<kModeFused>(x, ldx, rows, V, k, vals, idx, ws, st);
+  return dispatch_tma<kModeTopkOf>(x, ldx, rows, V, k, vals, idx, ws, st);
+}
+}  // namespace osmx_host

@@ -28,6 +28,7 @@ def lib():
     yield _lib
     _lib.config_set("shape", 0)
     _lib.config_set("split_chunk", 0)
+    _lib.config_set("tma", 0)
 
 
 def _dev(x):
@@ -141,12 +142,17 @@ def _topk_ref(oracle_mod, op, x, k):
     return v, z
 
 
-@pytest.mark.parametrize("shape", ["auto", "stream", "split"])
+@pytest.mark.parametrize("shape", ["auto", "stream", "split", "tma"])
 @pytest.mark.parametrize("k", [1, 2, 5, 8, 13, 32])
 def test_online_fused_topk_parity(cuda, oracle_mod, lib, shape, k):
     """Alg. 4: indices bit-exact (ties to the lowest index), values 1e-5."""
     from paper_1805_02867_b200 import osmx
 
+    if shape == "tma":
+        lib.config_set("tma", 2)
+        shape = "auto"
+    else:
+        lib.config_set("tma", 0)
     lib.config_set("shape", SHAPES[shape])
     if shape == "split":
         lib.config_set("split_chunk", 2048)
@@ -164,12 +170,17 @@ def test_online_fused_topk_parity(cuda, oracle_mod, lib, shape, k):
             assert max_rel(vals.cpu().numpy(), rv) <= TOL
 
 
-@pytest.mark.parametrize("shape", ["auto", "split"])
+@pytest.mark.parametrize("shape", ["auto", "split", "tma"])
 @pytest.mark.parametrize("k", [1, 5, 16])
 def test_topk_of_parity(cuda, oracle_mod, lib, shape, k):
     """topk_of: values and indices bit-exact (kernels.hpp:72-83)."""
     from paper_1805_02867_b200 import osmx
 
+    if shape == "tma":
+        lib.config_set("tma", 2)
+        shape = "auto"
+    else:
+        lib.config_set("tma", 0)
     lib.config_set("shape", SHAPES[shape])
     if shape == "split":
         lib.config_set("split_chunk", 2048)
