@@ -16,7 +16,7 @@ HDRS = $(wildcard $(SRC_DIR)/*.cuh) $(SRC_DIR)/internal.hpp include/osmx_b200.h
 OBJS = $(patsubst $(SRC_DIR)/%.cu,build/%.o,$(SRCS))
 LIB = paper_1805_02867_b200/libosmx_b200.so
 
-all: $(LIB) oracle
+all: $(LIB) oracle cxxtest
 
 build/%.o: $(SRC_DIR)/%.cu $(HDRS)
 	@mkdir -p build
@@ -33,3 +33,14 @@ clean:
 	$(MAKE) -s -C oracle clean
 
 .PHONY: all oracle clean
+
+# C++ API test (reference test cases through include/osmx/b200.hpp)
+CXXTEST = build/test_reference_api
+$(CXXTEST): tests/cpp/test_reference_api.cpp include/osmx/b200.hpp include/osmx_b200.h $(LIB) oracle
+	@mkdir -p build
+	g++ -std=c++20 -O2 -Wall -Iinclude -o $@ $< -L paper_1805_02867_b200 -losmx_b200 \
+	    -L oracle/_build -losmx_oracle -Wl,-rpath,'$$ORIGIN/../paper_1805_02867_b200' \
+	    -Wl,-rpath,'$$ORIGIN/../oracle/_build' -L/usr/local/cuda/lib64 -lcudart
+
+cxxtest: $(CXXTEST)
+.PHONY: cxxtest

@@ -59,6 +59,16 @@ def algo_bytes(alg: str, rows: int, V: int, k: int = K_TOP) -> int:
     return rows * per
 
 
+def kernel_name(rows: int, V: int) -> str:
+    """The fused top-K kernel the launch layer picks (topk_row_threads in
+    csrc/topk_impl.cuh) for this shape on a 148-SM B200."""
+    if V <= 2048 or rows >= 16 * 148:
+        return "k_topk_rows<32,256,5,kModeFused,4,4> (warp per row)"
+    if rows >= 4 * 148:
+        return "k_topk_rows<128,128,5,kModeFused,4,8>"
+    return "k_topk_rows<256,256,5,kModeFused,4,4>"
+
+
 def measured_peaks() -> dict:
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -354,7 +364,7 @@ def main() -> None:
         "clocks": clocks,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": None,
-                     "kernel": "k_topk_rows<256,256,5,kModeFused,4>",
+                     "kernel": kernel_name(rows, V),
                      "algorithmic_bytes_per_launch": bytes_launch,
                      "avg_launch_ms": round(kernel_ms, 4), "peak_source": peaks["source"]},
         "parity": parity,

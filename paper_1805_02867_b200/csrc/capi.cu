@@ -369,6 +369,10 @@ struct HostCtx {
 
 HostCtx g_ctx[64];
 
+// The second output block (int64 indices) starts 256-byte aligned after the
+// first (rpb*k floats): int64 stores need 8-byte alignment.
+size_t out2_offset(long long rpb, size_t out_row_bytes) { return ((size_t)rpb * out_row_bytes + 255) / 256 * 256; }
+
 template <class Launch>
 osmx_status host_pipeline(int device, long long rows, long long V, size_t out_row_bytes, int alg, int k,
                           const float* x, void* out_host, Launch&& launch, int64_t* first_bad_row,
@@ -385,7 +389,7 @@ osmx_status host_pipeline(int device, long long rows, long long V, size_t out_ro
   long long rpb = (long long)std::max<size_t>(1, budget / row_b);
   rpb = std::min(rpb, rows);
   const size_t out_tot = (out_row_bytes + out2_row_bytes);
-  e = c.ensure(rpb * row_b, std::max<size_t>(rpb * out_tot, 256),
+  e = c.ensure(rpb * row_b, std::max<size_t>(rpb * out_tot + 512, 256),
                workspace_bytes(alg, rpb, V, k));
   if (e != cudaSuccess) {
     cudaSetDevice(prev);
@@ -409,7 +413,7 @@ osmx_status host_pipeline(int device, long long rows, long long V, size_t out_ro
                           cudaMemcpyDeviceToHost, c.st[s]);
     if (e == cudaSuccess && out2_host)
       e = cudaMemcpyAsync(static_cast<char*>(out2_host) + r0 * out2_row_bytes,
-                          static_cast<char*>(c.out[s]) + (size_t)rpb * out_row_bytes, (size_t)nr * out2_row_bytes,
+                          static_cast<char*>(c.out[s]) + out2_offset(rpb, out_row_bytes), (size_t)nr * out2_row_bytes,
                           cudaMemcpyDeviceToHost, c.st[s]);
     if (e != cudaSuccess) st = cuda_status(e);
   }
@@ -479,7 +483,7 @@ osmx_status osmx_softmax_topk_host(int alg, const float* x, int64_t rows, int64_
         long long rpb = (long long)std::max<size_t>(1, budget / ((size_t)V * sizeof(float)));
         rpb = std::min<long long>(rpb, rows);
         float* dv = static_cast<float*>(dout);
-        long long* di = reinterpret_cast<long long*>(static_cast<char*>(dout) + (size_t)rpb * vb);
+        long long* di = reinterpret_cast<long long*>(static_cast<char*>(dout) + out2_offset(rpb, vb));
         osmx_status r = run_topk_alg(alg, dx, V, nr, V, k, dv, di, ws, wsb, st);
         return r == OSMX_OK ? cudaSuccess : (r == OSMX_ERR_CUDA ? cudaErrorUnknown : cudaErrorInvalidValue);
       },
@@ -502,7 +506,7 @@ osmx_status osmx_topk_host(const float* v, int64_t rows, int64_t V, int32_t k, f
         long long rpb = (long long)std::max<size_t>(1, budget / ((size_t)V * sizeof(float)));
         rpb = std::min<long long>(rpb, rows);
         float* dv = static_cast<float*>(dout);
-        long long* di = reinterpret_cast<long long*>(static_cast<char*>(dout) + (size_t)rpb * vb);
+        long long* di = reinterpret_cast<long long*>(static_cast<char*>(dout) + out2_offset(rpb, vb));
         osmx_status r = run_topk_alg(kTopkOf, dx, V, nr, V, k, dv, di, ws, wsb, st);
         return r == OSMX_OK ? cudaSuccess : (r == OSMX_ERR_CUDA ? cudaErrorUnknown : cudaErrorInvalidValue);
       },

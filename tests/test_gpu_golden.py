@@ -1,0 +1,139 @@
+"""GPU: the device path against the golden fixtures produced by the
+REFERENCE itself (tests/golden/make_golden.py), the V-split record combine
+on one device, the C++ reference-API test binary, and a full-size property
+check at the bench shape."""
+from __future__ import annotations
+
+import subprocess
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from tests._util import max_rel
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+GOLDEN = ROOT / "tests" / "golden" / "golden.npz"
+
+
+def _dev(x):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).cuda()
+
+
+@pytest.fixture(scope="module")
+def golden():
+    return np.load(GOLDEN)
+
+
+def test_device_vs_reference_golden(cuda, golden):
+    from paper_1805_02867_b200 import osmx
+
+    names = sorted({k.split("/")[0] for k in golden.files if "/x" in k})
+    for n in names:
+        x = golden[f"{n}/x"].reshape(1, -1)
+        k = int(golden[f"{n}/k"])
+        for alg in ("naive", "safe", "online"):
+            y = osmx.softmax(_dev(x), alg=alg).cpu().numpy()[0]
+            ref = golden[f"{n}/{alg}_softmax"]
+            fin = np.isfinite(ref)
+            assert np.array_equal(fin, np.isfinite(y)), (n, alg)
+            assert max_rel(y[fin], ref[fin]) <= 1e-5, (n, alg)
+        v, z = osmx.softmax_topk(_dev(x), k, alg="online_fused")
+        assert np.array_equal(z.cpu().numpy()[0], golden[f"{n}/online_softmax_topk/indices"]), n
+        assert max_rel(v.cpu().numpy()[0], golden[f"{n}/online_softmax_topk/values"]) <= 1e-5
+        v, z = osmx.topk(_dev(x), k)
+        assert np.array_equal(z.cpu().numpy()[0], golden[f"{n}/topk_of/indices"]), n
+        assert np.array_equal(v.cpu().numpy()[0], golden[f"{n}/topk_of/values"])
+        for alg, op in (("safe_fused", "safe_softmax_fused_topk"), ("safe_unfused", "safe_softmax_then_topk")):
+            v, z = osmx.softmax_topk(_dev(x), k, alg=alg)
+            gz = golden[f"{n}/{op}/indices"]
+            gv = golden[f"{n}/{op}/values"]
+            got = z.cpu().numpy()[0]
+            if not np.array_equal(got, gz):  # only probability-rounding collisions allowed
+                ys = golden[f"{n}/safe_softmax"]
+                assert np.allclose(np.sort(ys[got]), np.sort(ys[gz]), rtol=2.5e-7, atol=0), (n, alg)
+            assert max_rel(v.cpu().numpy()[0], gv) <= 1e-5
+        m, d = osmx.normalizer(_dev(x))
+        gm, gd = golden[f"{n}/run_normalizer_double"]
+        assert float(m[0]) == np.float32(gm)
+        assert abs(float(d[0]) - gd) <= 1e-5 * gd
+
+
+@pytest.mark.parametrize("k", [0, 1, 5, 32])
+def test_vsplit_records_on_one_device(cuda, oracle_mod, k):
+    """The cross-GPU combine (records of column slices merged in rank order)
+    exercised with several slices on one device."""
+    import torch
+
+    from paper_1805_02867_b200 import osmx
+
+    rng = np.random.default_rng(9 + k)
+    V = 300_001
+    x = rng.standard_normal(V).astype(np.float32)
+    x[7] = x[250_000] = 8.5  # a tie straddling slices
+    from paper_1805_02867_b200.shard import col_range
+
+    world = 5
+    xd = _dev(x)
+    recs = []
+    for r in range(world):
+        c0, c1 = col_range(V, world, r)
+        recs.append(osmx.slice_record(xd[c0:c1].reshape(1, -1), c0, k))
+    R = torch.stack(recs)
+    vals, idx, merged = osmx.records_combine(R, k)
+    if k > 0:
+        rv, rz, st = oracle_mod.topk("online_softmax_topk", x, k)
+        assert np.array_equal(idx.cpu().numpy(), rz)
+        assert max_rel(vals.cpu().numpy(), rv) <= 1e-5
+    ys = []
+    for r in range(world):
+        c0, c1 = col_range(V, world, r)
+        ys.append(osmx.scale_with_record(xd[c0:c1].reshape(1, -1), merged).cpu().numpy().reshape(-1))
+    y = np.concatenate(ys)
+    ry, _ = oracle_mod.softmax("online_softmax", x)
+    assert max_rel(y, ry) <= 1e-5
+
+
+def test_cpp_reference_api_binary(cuda):
+    exe = ROOT / "build" / "test_reference_api"
+    if not exe.exists():
+        subprocess.run(["make", "-C", str(ROOT), "cxxtest"], check=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600)
+    print(r.stdout[-2000:], r.stderr[-4000:])
+    assert r.returncode == 0 and "ALL OK" in r.stdout
+
+
+def test_bench_shape_properties(cuda, oracle_mod):
+    """At the full C4 row length: sampled rows bit-exact against the oracle,
+    and size-independent properties on all rows (values sorted, sum <= 1,
+    indices in range and distinct, top-1 == argmax of the row)."""
+    import torch
+
+    from paper_1805_02867_b200 import osmx
+
+    rows, V, k = 2048, 131072, 5
+    g = torch.Generator(device="cuda")
+    g.manual_seed(5)
+    x = torch.empty((rows, V), device="cuda").normal_(generator=g)
+    vals, idx = osmx.softmax_topk(x, k)
+    v = vals.cpu().numpy()
+    z = idx.cpu().numpy()
+    assert (np.diff(v, axis=1) <= 0).all()
+    assert (v.sum(axis=1) <= 1 + 1e-5).all()
+    assert ((z >= 0) & (z < V)).all()
+    assert all(len(set(r)) == k for r in z)
+    assert np.array_equal(z[:, 0], torch.argmax(x, dim=1).cpu().numpy())
+    sample = [0, 1, 777, rows - 1]
+    xs = x[sample].cpu().numpy()
+    rv, rz, _ = oracle_mod.batch("online_softmax_topk", xs, k=k)
+    assert np.array_equal(z[sample], rz)
+    assert max_rel(v[sample], rv) <= 1e-5
+    # the same rows through online softmax: sum-to-one and parity
+    y = osmx.softmax(x[:64], alg="online")
+    s = y.double().sum(dim=1).cpu().numpy()
+    assert np.allclose(s, 1.0, atol=1e-5)
+    ry, _ = oracle_mod.batch("online_softmax", x[:4].cpu().numpy())
+    assert max_rel(y[:4].cpu().numpy(), ry) <= 1e-5
