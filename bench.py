@@ -194,7 +194,7 @@ def run_reference_arm(args) -> None:
     per_row = t_probe / probe_rows
     total_steps = args.steps + args.warmup
     budget_s = 150.0
-    rows_sample = int(max(16, min(args.rows, budget_s / max(total_steps, 1) / per_row)))
+    rows_sample = int(max(16, min(args.rows, 8192, budget_s / max(total_steps, 1) / per_row)))
     xs = host_rows(1234, rows_sample, V)
     times = []
     for i in range(total_steps):
