@@ -62,9 +62,9 @@ def algo_bytes(alg: str, rows: int, V: int, k: int = K_TOP) -> int:
 def kernel_name(rows: int, V: int) -> str:
     """The fused top-K kernel the launch layer picks (topk_row_threads in
     csrc/topk_impl.cuh) for this shape on a 148-SM B200."""
-    if V <= 2048 or rows >= 16 * 148:
+    if V <= 2048 or rows >= 12 * 148:
         return "k_topk_rows<32,256,5,kModeFused,4,4> (warp per row)"
-    if rows >= 4 * 148:
+    if rows >= 2 * 148:
         return "k_topk_rows<128,128,5,kModeFused,4,8>"
     return "k_topk_rows<256,256,5,kModeFused,4,4>"
 

@@ -285,9 +285,6 @@ osmx_status osmx_config_set(const char* key, int64_t value) {
   } else if (!strcmp(key, "topk_threads")) {
     if (value != 0 && value != 32 && value != 128 && value != 256 && value != 512) return OSMX_ERR_INVALID_ARG;
     t.topk_threads = (int)value;
-  } else if (!strcmp(key, "topk_unroll")) {
-    if (value != 4 && value != 8) return OSMX_ERR_INVALID_ARG;
-    t.topk_unroll = (int)value;
   } else if (!strcmp(key, "tma")) {
     if (value < 0 || value > 2) return OSMX_ERR_INVALID_ARG;
     t.tma = (int)value;
@@ -309,7 +306,6 @@ int64_t osmx_config_get(const char* key) {
   if (!strcmp(key, "stream_threads")) return t.stream_threads;
   if (!strcmp(key, "topk_threads")) return t.topk_threads;
   if (!strcmp(key, "tma")) return t.tma;
-  if (!strcmp(key, "topk_unroll")) return t.topk_unroll;
   if (!strcmp(key, "host_chunk_mb")) return g_host_chunk_mb;
   return -1;
 }

@@ -32,13 +32,12 @@ enum Shape : int {
 
 struct Tuning {
   int shape = kShapeAuto;       // force a family (0 = heuristic)
-  int resident_max_v = 16384;   // largest V held in registers
+  int resident_max_v = 8192;    // largest V held in registers (128-bit rows)
   long long split_chunk = 0;    // elements per CTA in split mode (0 = auto)
   int stream_threads = 0;       // CTA size for stream kernels (0 = auto)
   int topk_threads = 0;         // CTA size for the fused top-K (0 = auto)
   int tma = 0;                  // TMA-ring top-K: 0 off (default: the warp-per-row
                                 // LDG kernel measures faster), 1 auto, 2 force
-  int topk_unroll = 4;          // float4s in flight per thread in the row top-K (4, 8)
 };
 Tuning& tuning();
 
@@ -76,6 +75,7 @@ size_t workspace_bytes(int alg, long long rows, long long V, int k);
 
 // softmax.cu
 size_t softmax_split_ws(long long rows, long long V);
+int resident_limit(bool vec);  // largest V for the resident family
 bool softmax_uses_split(long long rows, long long V);
 // Safe split phases 0 and 1 (row max, then d against it) into 16-byte
 // records {float m, float mn, double d} (the safe fused top-K's first passes).

@@ -15,11 +15,17 @@ size_t softmax_split_ws(long long rows, long long V) {
   return (size_t)(rows * S) * sizeof(SRec);
 }
 
+int resident_limit(bool vec) {
+  const int r = tuning().resident_max_v;
+  return vec ? r : std::min(r, 4096);
+}
+
+// Conservative (workspace sizing does not know the pointers' alignment).
 bool softmax_uses_split(long long rows, long long V) {
   const auto& tn = tuning();
   if (tn.shape == kShapeSplit) return rows <= 65535;
   if (tn.shape != kShapeAuto) return false;
-  return V > tn.resident_max_v && rows < 2LL * num_sms();
+  return V > resident_limit(false) && rows < 2LL * num_sms();
 }
 
 cudaError_t launch_softmax(int alg, const float* x, long long ldx, float* y, long long ldy,

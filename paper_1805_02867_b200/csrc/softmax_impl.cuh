@@ -626,9 +626,15 @@ template <int ALG>
 cudaError_t launch_alg(const float* x, long long ldx, float* y, long long ldy, long long rows,
                        long long V, void* ws, cudaStream_t st) {
   const auto& tn = osmx_host::tuning();
+  const bool vec = (V % 4 == 0) && (ldx % 4 == 0) && (ldy % 4 == 0) &&
+                   ((reinterpret_cast<uintptr_t>(x) & 15u) == 0) && ((reinterpret_cast<uintptr_t>(y) & 15u) == 0);
   int shape = tn.shape;
   if (shape == osmx_host::kShapeAuto) {
-    if (V <= tn.resident_max_v)
+    // Measured on B200 (tools/shape_sweep.py, cold L2, 4000 rows): the
+    // register-resident rows win up to V = 8192 with 128-bit loads; rows that
+    // cannot use them (V % 4 != 0 / unaligned) only up to ~4096; beyond that
+    // the two-pass stream kernel (second pass from L2) is faster.
+    if (V <= osmx_host::resident_limit(vec))
       shape = osmx_host::kShapeResident;
     else if (rows >= 2LL * osmx_host::num_sms())
       shape = osmx_host::kShapeStream;
@@ -636,12 +642,8 @@ cudaError_t launch_alg(const float* x, long long ldx, float* y, long long ldy, l
       shape = osmx_host::kShapeSplit;
   }
   if (shape == osmx_host::kShapeResident && V > 16384) shape = osmx_host::kShapeStream;
-  if (shape == osmx_host::kShapeResident) {
-    const bool vec = (V % 4 == 0) && (ldx % 4 == 0) && (ldy % 4 == 0) &&
-                     ((reinterpret_cast<uintptr_t>(x) & 15u) == 0) &&
-                     ((reinterpret_cast<uintptr_t>(y) & 15u) == 0);
-    return dispatch_resident<ALG>(vec, x, ldx, y, ldy, rows, V, ws, st);
-  }
+  if (shape == osmx_host::kShapeSplit && rows > 65535) shape = osmx_host::kShapeStream;
+  if (shape == osmx_host::kShapeResident) return dispatch_resident<ALG>(vec, x, ldx, y, ldy, rows, V, ws, st);
   if (shape == osmx_host::kShapeSplit) return run_split<ALG>(x, ldx, y, ldy, rows, V, ws, st);
   return run_stream<ALG>(x, ldx, y, ldy, rows, V, ws, st);
 }

@@ -235,7 +235,7 @@ __device__ __forceinline__ void cta_merge(TopList<KC>& L, int k, float* sv, int*
 // ---------------------------------------------------------- row kernel --
 // G threads per row (G == 32: warp per row, BLOCK/32 rows per CTA; G ==
 // BLOCK: CTA per row).  Rows are visited grid-stride.
-template <int G, int BLOCK, int KC, int MODE, int U, int MINB = 1>
+template <int G, int BLOCK, int KC, int MODE, int U, int MINB>
 __global__ void __launch_bounds__(BLOCK, MINB)
     k_topk_rows(const float* __restrict__ x, long long ldx, long long rows, long long V, int k,
                 float* __restrict__ vals, long long* __restrict__ idx, void* ws) {
@@ -468,8 +468,14 @@ inline int topk_row_threads(long long rows, long long V) {
   const long long sms = osmx_host::num_sms();
   // measured on B200 (profiles/): warp-per-row reads C4 at 7.1 TB/s vs 6.5
   // (128 threads) and 5.9 (256); it wins down to ~4000 rows.
-  if (V <= 2048 || rows >= 16 * sms) return 32;
-  if (rows >= 4 * sms) return 128;
+  // 4000 rows: warp/row 4.7-7.0 TB/s vs 3.5-6.5 (128 thr); 1000 rows: 128 thr
+  // 2.9-4.8 TB/s vs 1.6-2.3 (warp/row) -- tools/shape_sweep.py, cold L2.
+  // Also measured and rejected for the warp-per-row kernel: 8 float4s in
+  // flight (73 regs, -20%), software-pipelined next-batch loads (80 regs,
+  // -20% at 4000 rows: fewer resident warps than rows), a 48/40-register
+  // cap (spills; -0..-30%).
+  if (V <= 2048 || rows >= 12 * sms) return 32;
+  if (rows >= 2 * sms) return 128;
   return 256;
 }
 
