@@ -382,7 +382,7 @@ def main() -> None:
     # ---- e2e through the host-buffer C-ABI entry point (pinned host rows)
     do_e2e = args.e2e == "on" or (args.e2e == "auto")
     if do_e2e:
-        result["e2e"] = e2e_measure(lib, _lib, x, rows, V, k, dev, world, dist, local)
+        result["e2e"] = e2e_measure(lib, _lib, x, idx, rows, V, k, dev, world, dist, local)
 
     # ---- CPU baseline (rank 0, N=1)
     if rank == 0 and world == 1 and args.cpu != "off":
@@ -400,7 +400,7 @@ def main() -> None:
         dist.destroy_process_group()
 
 
-def e2e_measure(lib, _lib, x, rows, V, k, dev, world, dist, local) -> dict:
+def e2e_measure(lib, _lib, x, dev_idx, rows, V, k, dev, world, dist, local) -> dict:
     import ctypes as C
 
     import numpy as np
@@ -438,7 +438,8 @@ def e2e_measure(lib, _lib, x, rows, V, k, dev, world, dist, local) -> dict:
         tt = torch.tensor([t], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t = float(tt[0])
-    ok = bool(np.array_equal(hi[:4].numpy(), hi[:4].numpy()))
+    # the host-buffer path must return what the device-resident launch returned
+    ok = bool(np.array_equal(hi.numpy(), dev_idx[:e_rows].cpu().numpy()))
     lib.osmx_host_release()
     gbs = algo_bytes("online_fused", e_rows * world, V, k) / t / 1e9
     return {"value": round(gbs, 2), "unit": "GB/s", "h2d_bytes_per_step": e_rows * V * 4,
@@ -463,63 +464,97 @@ def cpu_baseline(x, V, k) -> dict:
             "seconds": round(t, 3), "rows_per_s": round(n / t, 2), "elements_per_s": round(n * V / t, 1)}
 
 
+def time_rotating(launch, n_sets: int, reps: int, graph: bool = True):
+    """Per-launch device time of `launch(i, stream_handle)` over n_sets
+    distinct buffer sets launched back to back (set i's inputs were last
+    touched n_sets-1 launches ago, so with n_sets * working set >= 4 x L2
+    every launch starts with its inputs out of L2).  The n_sets launches are
+    captured in one CUDA graph (no host launch gaps), timed with CUDA events
+    on the launching stream; returns (median ms per launch, min ms)."""
+    import torch
+
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for i in range(n_sets):  # warm-up (and first-touch of every set)
+            launch(i, s.cuda_stream)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = None
+    if graph:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for i in range(n_sets):
+                launch(i, s.cuda_stream)
+        torch.cuda.synchronize()
+    ts = []
+    with torch.cuda.stream(s):
+        for _ in range(reps):
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(s)
+            if g is not None:
+                g.replay()
+            else:
+                for i in range(n_sets):
+                    launch(i, s.cuda_stream)
+            b.record(s)
+            b.synchronize()
+            ts.append(a.elapsed_time(b) / n_sets)
+    torch.cuda.synchronize()
+    return statistics.median(ts), min(ts)
+
+
+def n_rotating_sets(set_bytes: int, l2: int, cap_bytes: int = 48 << 30) -> int:
+    """Buffer sets so that the rotation covers >= 4 x L2 (at least 2)."""
+    n = max(2, -(-4 * l2 // max(set_bytes, 1)))
+    return int(max(2, min(n, cap_bytes // max(set_bytes, 1))))
+
+
 def run_sweeps(lib, _lib, dev, sp, reps, peak) -> dict:
     """configs[1]: safe vs online softmax, batch 4000, V = log_spaced(10, 1e6, 21).
     configs[2]: fused online softmax+Top-5 vs unfused online->TopK, batch 4000,
-    V = 32K..1M.  Cold L2 (a 256 MB buffer is written between repeats) when
-    the working set is < 2x L2; kernel-only CUDA-event timing, median."""
+    V = 32K..1M.  Every launch reads inputs that are out of L2: launches
+    rotate over >= 2 buffer sets covering >= 4 x L2, captured in one CUDA
+    graph and timed with CUDA events (time_rotating); median of `reps`."""
     import torch
 
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     B = 4000
     k = K_TOP
-
-    def time_op(fn, ws_bytes_in_flight):
-        cold = ws_bytes_in_flight < 2 * l2
-        for _ in range(2):
-            fn()
-        ts = []
-        for _ in range(reps):
-            if cold:
-                flush.fill_(1)
-            a = torch.cuda.Event(enable_timing=True)
-            b = torch.cuda.Event(enable_timing=True)
-            a.record()
-            fn()
-            b.record()
-            b.synchronize()
-            ts.append(a.elapsed_time(b))
-        return statistics.median(ts), cold
-
-    out = {"batch": B, "k": k, "softmax": [], "topk": []}
+    out = {"batch": B, "k": k, "timing": "CUDA graph of n_sets launches over rotating buffer sets "
+                                          "(>= 4 x L2, inputs cold in L2), CUDA events, median",
+           "softmax": [], "topk": []}
     Vs = [10, 18, 32, 56, 100, 178, 316, 562, 1000, 1778, 3162, 5623, 10000, 17783, 31623, 56234, 100000, 177828,
           316228, 562341, 1000000]
     for V in Vs:
-        x = torch.empty((B, V), dtype=torch.float32, device=dev).normal_()
+        n = n_rotating_sets(8 * B * V, l2)
+        x = torch.empty((n, B, V), dtype=torch.float32, device=dev).normal_()
         y = torch.empty_like(x)
-        row = {"V": V}
-        for name, alg in (("safe", _lib.SAFE_SOFTMAX), ("online", _lib.ONLINE_SOFTMAX)):
+        row = {"V": V, "n_sets": n}
+        for name, alg in (("naive", _lib.NAIVE_SOFTMAX), ("safe", _lib.SAFE_SOFTMAX),
+                          ("online", _lib.ONLINE_SOFTMAX)):
             nb = lib.osmx_workspace_bytes(alg, B, V, 0)
             ws = torch.zeros(max(nb, 256), dtype=torch.uint8, device=dev)
 
-            def fn():
-                lib.osmx_softmax(alg, x.data_ptr(), V, y.data_ptr(), V, B, V, ws.data_ptr(), ws.numel(), sp)
+            def launch(i, st, alg=alg, ws=ws):
+                lib.osmx_softmax(alg, x[i].data_ptr(), V, y[i].data_ptr(), V, B, V, ws.data_ptr(), ws.numel(), st)
 
-            ms, cold = time_op(fn, 8 * B * V)
+            ms, ms_min = time_rotating(launch, n, reps)
             gbs = algo_bytes(name, B, V) / (ms * 1e-3) / 1e9
-            row[name] = {"ms": round(ms, 4), "GBps": round(gbs, 1), "frac": round(gbs / peak, 3),
+            row[name] = {"ms": round(ms, 5), "GBps": round(gbs, 1), "frac": round(gbs / peak, 3),
                          "dram_floor_GBps": round(8 * B * V / (ms * 1e-3) / 1e9, 1),
                          "elements_per_s": round(B * V / (ms * 1e-3), 1)}
-            row["cold_l2"] = cold
         row["online_over_safe"] = round(row["safe"]["ms"] / row["online"]["ms"], 3)
         out["softmax"].append(row)
         del x, y
+        torch.cuda.empty_cache()
     for V in [32768, 65536, 131072, 262144, 524288, 1048576]:
-        x = torch.empty((B, V), dtype=torch.float32, device=dev).normal_()
+        n = n_rotating_sets(4 * B * V, l2)
+        x = torch.empty((n, B, V), dtype=torch.float32, device=dev).normal_()
         vals = torch.empty((B, k), dtype=torch.float32, device=dev)
         idx = torch.empty((B, k), dtype=torch.int64, device=dev)
-        row = {"V": V}
+        row = {"V": V, "n_sets": n}
         for name, alg in (("online_fused", _lib.ONLINE_SOFTMAX_FUSED_TOPK),
                           ("online_unfused", _lib.ONLINE_SOFTMAX_UNFUSED_TOPK),
                           ("safe_unfused", _lib.SAFE_SOFTMAX_UNFUSED_TOPK),
@@ -527,20 +562,20 @@ def run_sweeps(lib, _lib, dev, sp, reps, peak) -> dict:
             nb = lib.osmx_workspace_bytes(alg, B, V, k)
             ws = torch.zeros(max(nb, 256), dtype=torch.uint8, device=dev)
 
-            def fn():
-                lib.osmx_softmax_topk(alg, x.data_ptr(), V, B, V, k, vals.data_ptr(), idx.data_ptr(), ws.data_ptr(),
-                                      ws.numel(), sp)
+            def launch(i, st, alg=alg, ws=ws):
+                lib.osmx_softmax_topk(alg, x[i].data_ptr(), V, B, V, k, vals.data_ptr(), idx.data_ptr(),
+                                      ws.data_ptr(), ws.numel(), st)
 
-            ms, cold = time_op(fn, 4 * B * V)
+            ms, ms_min = time_rotating(launch, n, reps)
             gbs = algo_bytes(name, B, V) / (ms * 1e-3) / 1e9
-            row[name] = {"ms": round(ms, 4), "GBps": round(gbs, 1), "frac": round(gbs / peak, 3),
+            row[name] = {"ms": round(ms, 5), "GBps": round(gbs, 1), "frac": round(gbs / peak, 3),
                          "rows_per_s": round(B / (ms * 1e-3), 1)}
             del ws
         row["fused_over_online_unfused"] = round(row["online_unfused"]["ms"] / row["online_fused"]["ms"], 3)
         row["fused_over_safe_unfused"] = round(row["safe_unfused"]["ms"] / row["online_fused"]["ms"], 3)
         out["topk"].append(row)
         del x
-    torch.cuda.empty_cache()
+        torch.cuda.empty_cache()
     return out
 
 

@@ -271,7 +271,7 @@ osmx_status osmx_config_set(const char* key, int64_t value) {
   if (!key) return OSMX_ERR_INVALID_ARG;
   auto& t = tuning();
   if (!strcmp(key, "shape")) {
-    if (value < 0 || value > 3) return OSMX_ERR_INVALID_ARG;
+    if (value < 0 || value > 4) return OSMX_ERR_INVALID_ARG;
     t.shape = (int)value;
   } else if (!strcmp(key, "resident_max_v")) {
     if (value < 0 || value > 16384) return OSMX_ERR_INVALID_ARG;
@@ -285,6 +285,12 @@ osmx_status osmx_config_set(const char* key, int64_t value) {
   } else if (!strcmp(key, "topk_threads")) {
     if (value != 0 && value != 32 && value != 128 && value != 256 && value != 512) return OSMX_ERR_INVALID_ARG;
     t.topk_threads = (int)value;
+  } else if (!strcmp(key, "topk_u8")) {
+    if (value < -1 || value > 1) return OSMX_ERR_INVALID_ARG;
+    t.topk_u8 = (int)value;
+  } else if (!strcmp(key, "l2_prefetch")) {
+    if (value < 0 || value > 64) return OSMX_ERR_INVALID_ARG;
+    t.l2_prefetch = (int)value;
   } else if (!strcmp(key, "tma")) {
     if (value < 0 || value > 2) return OSMX_ERR_INVALID_ARG;
     t.tma = (int)value;
@@ -306,6 +312,8 @@ int64_t osmx_config_get(const char* key) {
   if (!strcmp(key, "stream_threads")) return t.stream_threads;
   if (!strcmp(key, "topk_threads")) return t.topk_threads;
   if (!strcmp(key, "tma")) return t.tma;
+  if (!strcmp(key, "l2_prefetch")) return t.l2_prefetch;
+  if (!strcmp(key, "topk_u8")) return t.topk_u8;
   if (!strcmp(key, "host_chunk_mb")) return g_host_chunk_mb;
   return -1;
 }

@@ -28,6 +28,7 @@ enum Shape : int {
   kShapeResident = 1,  // row held in registers by a group of <= 1024 threads
   kShapeStream = 2,    // one CTA per row, every pass streams global memory
   kShapeSplit = 3,     // row split over S CTAs, (m,d)/top-K records + combine
+  kShapeStaged = 4,    // rows staged in a TMA-fed shared-memory ring (persistent)
 };
 
 struct Tuning {
@@ -36,6 +37,8 @@ struct Tuning {
   long long split_chunk = 0;    // elements per CTA in split mode (0 = auto)
   int stream_threads = 0;       // CTA size for stream kernels (0 = auto)
   int topk_threads = 0;         // CTA size for the fused top-K (0 = auto)
+  int topk_u8 = -1;             // warp-per-row top-K with 8 float4s in flight (-1 auto)
+  int l2_prefetch = 0;          // bulk L2 prefetch distance in batches (0 = off)
   int tma = 0;                  // TMA-ring top-K: 0 off (default: the warp-per-row
                                 // LDG kernel measures faster), 1 auto, 2 force
 };

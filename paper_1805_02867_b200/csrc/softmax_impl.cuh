@@ -25,6 +25,7 @@
 
 #include "common.cuh"
 #include "internal.hpp"
+#include "softmax_staged.cuh"
 #include "stream.cuh"
 
 using namespace osmx_dev;
@@ -221,7 +222,7 @@ __global__ void __launch_bounds__(TPR > 256 ? TPR : 256)
 template <int BLOCK, int U, int ALG>
 __global__ void __launch_bounds__(BLOCK)
     k_softmax_stream(const float* __restrict__ x, long long ldx, float* __restrict__ y,
-                     long long ldy, long long rows, long long V, void* ws) {
+                     long long ldy, long long rows, long long V, void* ws, int pf) {
   constexpr int NW = BLOCK / 32;
   __shared__ float smf[2 * NW];
   __shared__ double smd[NW];
@@ -252,7 +253,8 @@ __global__ void __launch_bounds__(BLOCK)
             mn = fminf(mn, bn);
             acc.raise(bm);
             acc.add_batch<U>(v);
-          });
+          },
+          pf);
       MD tot = md_cta_reduce<NW>(acc.finish(), smf);
       mn = cta_min<NW>(mn, smf);
       M = tot.m;
@@ -274,7 +276,8 @@ __global__ void __launch_bounds__(BLOCK)
               m = fmaxf(m, fmaxf(fmaxf(v[u].x, v[u].y), fmaxf(v[u].z, v[u].w)));
               if (u < cnt) mn = fminf(mn, fminf(fminf(v[u].x, v[u].y), fminf(v[u].z, v[u].w)));
             }
-          });
+          },
+          pf);
       M = cta_max<NW>(m, smf);
       mn = cta_min<NW>(mn, smf);
       L2Acc sacc;  // sum e^(x - M) as one FFMA + ex2 per element
@@ -576,14 +579,15 @@ template <int ALG>
 cudaError_t run_stream(const float* x, long long ldx, float* y, long long ldy, long long rows,
                        long long V, void* ws, cudaStream_t st) {
   int threads = osmx_host::tuning().stream_threads;
+  const int pf = osmx_host::tuning().l2_prefetch;
   if (threads == 0) threads = V >= 65536 ? 512 : 256;
   const long long grid = std::min<long long>(rows, 1LL << 30);
   if (threads == 1024)
-    k_softmax_stream<1024, 4, ALG><<<(unsigned)grid, 1024, 0, st>>>(x, ldx, y, ldy, rows, V, ws);
+    k_softmax_stream<1024, 4, ALG><<<(unsigned)grid, 1024, 0, st>>>(x, ldx, y, ldy, rows, V, ws, pf);
   else if (threads == 512)
-    k_softmax_stream<512, 4, ALG><<<(unsigned)grid, 512, 0, st>>>(x, ldx, y, ldy, rows, V, ws);
+    k_softmax_stream<512, 4, ALG><<<(unsigned)grid, 512, 0, st>>>(x, ldx, y, ldy, rows, V, ws, pf);
   else
-    k_softmax_stream<256, 4, ALG><<<(unsigned)grid, 256, 0, st>>>(x, ldx, y, ldy, rows, V, ws);
+    k_softmax_stream<256, 4, ALG><<<(unsigned)grid, 256, 0, st>>>(x, ldx, y, ldy, rows, V, ws, pf);
   osmx_host::count_launch();
   return cudaGetLastError();
 }
@@ -642,6 +646,10 @@ cudaError_t launch_alg(const float* x, long long ldx, float* y, long long ldy, l
       shape = osmx_host::kShapeSplit;
   }
   if (shape == osmx_host::kShapeResident && V > 16384) shape = osmx_host::kShapeStream;
+  if (shape == osmx_host::kShapeStaged) {
+    if (V <= kStagedMaxV) return run_staged<ALG>(x, ldx, y, ldy, rows, V, ws, st);
+    shape = osmx_host::kShapeStream;
+  }
   if (shape == osmx_host::kShapeSplit && rows > 65535) shape = osmx_host::kShapeStream;
   if (shape == osmx_host::kShapeResident) return dispatch_resident<ALG>(vec, x, ldx, y, ldy, rows, V, ws, st);
   if (shape == osmx_host::kShapeSplit) return run_split<ALG>(x, ldx, y, ldy, rows, V, ws, st);

@@ -36,6 +36,12 @@ __device__ __forceinline__ Seg make_seg(const float* p, long long n) {
   return s;
 }
 
+// Bulk prefetch of [p, p + bytes) into L2 (no registers, no completion to
+// wait for): p 16-byte aligned, bytes a multiple of 16.
+__device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 // Element index of component c of body float4 q.
 __device__ __forceinline__ long long body_index(const Seg& s, long long q, int c) {
   return s.head + 4 * q + c;
@@ -45,12 +51,24 @@ __device__ __forceinline__ long long body_index(const Seg& s, long long q, int c
 //   f1(x, j)                    scalar element j
 //   fb(v[U], q0, cnt)           cnt (<= U) float4s at body indices q0 + u*G
 // LAST selects the evict-first load flavour (final read of the data).
+// pf > 0: thread 0 of the group keeps the group's body pf batches ahead in
+// L2 with bulk prefetches, so the demand loads see L2 rather than DRAM
+// latency without spending registers on more loads in flight.
 template <int G, int U, bool LAST, class F1, class FB>
-__device__ __forceinline__ void stream_seg(const Seg& s, int t, F1&& f1, FB&& fb) {
+__device__ __forceinline__ void stream_seg(const Seg& s, int t, F1&& f1, FB&& fb, int pf = 0) {
   if (t < s.head) f1(LAST ? ld_f1_last(s.p + t) : ld_f1(s.p + t), (long long)t);
   const float* b = s.p + s.head;
+  constexpr long long kB = (long long)U * G;  // float4s per batch of the group
+  if (pf > 0 && t == 0 && s.nvec > 0) {
+    const long long n = s.nvec < pf * kB ? s.nvec : pf * kB;
+    prefetch_l2(b, (unsigned)(16 * n));
+  }
   long long q = t;
   for (; q + (long long)(U - 1) * G < s.nvec; q += (long long)U * G) {
+    if (pf > 0 && t == 0) {
+      const long long qa = q + pf * kB;
+      if (qa < s.nvec) prefetch_l2(b + 4 * qa, (unsigned)(16 * (s.nvec - qa < kB ? s.nvec - qa : kB)));
+    }
     float4 v[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) v[u] = LAST ? ld_f4_last(b + 4 * (q + (long long)u * G)) : ld_f4(b + 4 * (q + (long long)u * G));

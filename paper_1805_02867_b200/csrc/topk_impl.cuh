@@ -197,10 +197,10 @@ __device__ __forceinline__ float safe_sum(const Seg& s, int t, float M) {
 }
 
 template <int G, int U, int KC, int MODE>
-__device__ __forceinline__ void run_pass(Pass<KC, U, MODE, G>& P, const Seg& s, int t, int k) {
+__device__ __forceinline__ void run_pass(Pass<KC, U, MODE, G>& P, const Seg& s, int t, int k, int pf = 0) {
   stream_seg<G, U, MODE == kModeSafe>(
       s, t, [&](float v, long long j) { P.scalar(v, (int)j, k); },
-      [&](float4 (&v)[U], long long q0, int cnt) { P.batch(s, v, q0, cnt, k); });
+      [&](float4 (&v)[U], long long q0, int cnt) { P.batch(s, v, q0, cnt, k); }, pf);
 }
 
 // Cross-warp merge for a CTA-wide group: each warp's k winners go to smem,
@@ -238,7 +238,7 @@ __device__ __forceinline__ void cta_merge(TopList<KC>& L, int k, float* sv, int*
 template <int G, int BLOCK, int KC, int MODE, int U, int MINB>
 __global__ void __launch_bounds__(BLOCK, MINB)
     k_topk_rows(const float* __restrict__ x, long long ldx, long long rows, long long V, int k,
-                float* __restrict__ vals, long long* __restrict__ idx, void* ws) {
+                float* __restrict__ vals, long long* __restrict__ idx, void* ws, int pf) {
   constexpr int NW = BLOCK / 32;
   constexpr int RPC = BLOCK / G;
   __shared__ float smf[2 * NW];
@@ -283,7 +283,7 @@ __global__ void __launch_bounds__(BLOCK, MINB)
       P.R = __frcp_rn(d);
       bad = !(d == d) || !isfinite(M) || !(MN == MN) || MN == kNegInf;
     }
-    run_pass<G, U, KC, MODE>(P, s, t, k);
+    run_pass<G, U, KC, MODE>(P, s, t, k, pf);
     if constexpr (MODE == kModeFused) {
       MD tot;
       float MN;
@@ -483,22 +483,33 @@ template <int KC, int MODE>
 cudaError_t run_rows(const float* x, long long ldx, long long rows, long long V, int k, float* vals,
                      long long* idx, void* ws, cudaStream_t st) {
   const int g = topk_row_threads(rows, V);
-  if (g == 32) {
+  const int pf = osmx_host::tuning().l2_prefetch;
+  int u8 = osmx_host::tuning().topk_u8;
+  // measured (tools/shape_sweep.py, 4000 rows): +8-9% at V = 16K-32K, +1% at
+  // 64K, -2% at 128K (rows long enough to amortise the serial load->compute).
+  if (u8 < 0) u8 = (g == 32 && V >= 8192 && V <= 65536 && rows <= 28LL * osmx_host::num_sms()) ? 1 : 0;
+  if (g == 32 && u8) {
+    // One wave of rows (<= 28 warps per SM): occupancy is set by the row
+    // count, not by registers, so each lane keeps 8 float4s in flight
+    // (4-warp CTAs, <= 72 registers: 7 CTAs = 28 warps per SM).
+    const long long grid = std::min<long long>((rows + 3) / 4, 1LL << 30);
+    k_topk_rows<32, 128, KC, MODE, 8, 7><<<(unsigned)grid, 128, 0, st>>>(x, ldx, rows, V, k, vals, idx, ws, pf);
+  } else if (g == 32) {
     constexpr int RPC = 256 / 32;
     const long long groups = (rows + RPC - 1) / RPC;
     const long long grid = std::min<long long>(groups, 1LL << 30);
     if (V <= 2048)
-      k_topk_rows<32, 256, KC, MODE, 2, 4><<<(unsigned)grid, 256, 0, st>>>(x, ldx, rows, V, k, vals, idx, ws);
+      k_topk_rows<32, 256, KC, MODE, 2, 4><<<(unsigned)grid, 256, 0, st>>>(x, ldx, rows, V, k, vals, idx, ws, pf);
     else
-      k_topk_rows<32, 256, KC, MODE, 4, 4><<<(unsigned)grid, 256, 0, st>>>(x, ldx, rows, V, k, vals, idx, ws);
+      k_topk_rows<32, 256, KC, MODE, 4, 4><<<(unsigned)grid, 256, 0, st>>>(x, ldx, rows, V, k, vals, idx, ws, pf);
   } else {
     const long long grid = std::min<long long>(rows, 1LL << 30);
     if (g == 128)
-      k_topk_rows<128, 128, KC, MODE, 4, 8><<<(unsigned)grid, 128, 0, st>>>(x, ldx, rows, V, k, vals, idx, ws);
+      k_topk_rows<128, 128, KC, MODE, 4, 8><<<(unsigned)grid, 128, 0, st>>>(x, ldx, rows, V, k, vals, idx, ws, pf);
     else if (g == 512)
-      k_topk_rows<512, 512, KC, MODE, 4, 2><<<(unsigned)grid, 512, 0, st>>>(x, ldx, rows, V, k, vals, idx, ws);
+      k_topk_rows<512, 512, KC, MODE, 4, 2><<<(unsigned)grid, 512, 0, st>>>(x, ldx, rows, V, k, vals, idx, ws, pf);
     else
-      k_topk_rows<256, 256, KC, MODE, 4, 4><<<(unsigned)grid, 256, 0, st>>>(x, ldx, rows, V, k, vals, idx, ws);
+      k_topk_rows<256, 256, KC, MODE, 4, 4><<<(unsigned)grid, 256, 0, st>>>(x, ldx, rows, V, k, vals, idx, ws, pf);
   }
   osmx_host::count_launch();
   return cudaGetLastError();

@@ -17,7 +17,13 @@ from tests._util import DISTS, dist, max_rel
 pytestmark = pytest.mark.gpu
 
 TOL = 1e-5
-SHAPES = {"auto": 0, "resident": 1, "stream": 2, "split": 3}
+SHAPES = {"auto": 0, "resident": 1, "stream": 2, "split": 3, "staged": 4}
+# top-K launch variants: knob settings applied on top of the shape
+TOPK_VARIANTS = {
+    "auto": [], "stream": [("shape", 2)], "split": [("shape", 3), ("split_chunk", 2048)], "tma": [("tma", 2)],
+    "warp": [("topk_threads", 32), ("topk_u8", 0)], "warp_u8": [("topk_threads", 32), ("topk_u8", 1)],
+    "warp_pf": [("topk_threads", 32), ("l2_prefetch", 2)], "cta_pf": [("topk_threads", 256), ("l2_prefetch", 1)],
+}
 
 
 @pytest.fixture
@@ -26,9 +32,9 @@ def lib():
 
     _lib.load()
     yield _lib
-    _lib.config_set("shape", 0)
-    _lib.config_set("split_chunk", 0)
-    _lib.config_set("tma", 0)
+    for key, val in (("shape", 0), ("split_chunk", 0), ("tma", 0), ("topk_threads", 0), ("topk_u8", -1),
+                     ("l2_prefetch", 0)):
+        _lib.config_set(key, val)
 
 
 def _dev(x):
@@ -40,7 +46,7 @@ def _dev(x):
 SOFTMAX_V = [1, 2, 3, 5, 10, 17, 32, 33, 100, 255, 256, 1000, 1023, 1025, 2048, 4099, 8192, 16384, 16387, 70001]
 
 
-@pytest.mark.parametrize("shape", ["auto", "resident", "stream", "split"])
+@pytest.mark.parametrize("shape", ["auto", "resident", "stream", "split", "staged"])
 @pytest.mark.parametrize("alg", ["naive", "safe", "online"])
 def test_softmax_parity(cuda, oracle_mod, lib, alg, shape):
     from paper_1805_02867_b200 import osmx
@@ -51,7 +57,7 @@ def test_softmax_parity(cuda, oracle_mod, lib, alg, shape):
     rng = np.random.default_rng(100 + SHAPES[shape])
     worst = 0.0
     for V in SOFTMAX_V:
-        if shape == "resident" and V > 16384:
+        if shape in ("resident", "staged") and V > 16384:
             continue
         for d in DISTS:
             if alg == "naive" and d in ("wide", "spikes", "quantized100"):
@@ -76,10 +82,10 @@ def test_softmax_strided_and_misaligned(cuda, oracle_mod, lib, alg):
     from paper_1805_02867_b200 import osmx
 
     rng = np.random.default_rng(7)
-    for shape in (0, 2, 3):
+    for shape in (0, 2, 3, 4):
         lib.config_set("shape", shape)
         lib.config_set("split_chunk", 4096 if shape == 3 else 0)
-        for V in (5, 999, 20001):
+        for V in (5, 999, 4097, 20001):
             big = rng.standard_normal((6, V + 7)).astype(np.float32)
             xt = torch.from_numpy(big).cuda()[:, 1 : V + 1]  # ld = V+7, base offset 4 bytes
             y = osmx.softmax(xt, alg=alg).cpu().numpy()
@@ -142,20 +148,14 @@ def _topk_ref(oracle_mod, op, x, k):
     return v, z
 
 
-@pytest.mark.parametrize("shape", ["auto", "stream", "split", "tma"])
+@pytest.mark.parametrize("shape", list(TOPK_VARIANTS))
 @pytest.mark.parametrize("k", [1, 2, 5, 8, 13, 32])
 def test_online_fused_topk_parity(cuda, oracle_mod, lib, shape, k):
     """Alg. 4: indices bit-exact (ties to the lowest index), values 1e-5."""
     from paper_1805_02867_b200 import osmx
 
-    if shape == "tma":
-        lib.config_set("tma", 2)
-        shape = "auto"
-    else:
-        lib.config_set("tma", 0)
-    lib.config_set("shape", SHAPES[shape])
-    if shape == "split":
-        lib.config_set("split_chunk", 2048)
+    for key, val in TOPK_VARIANTS[shape]:
+        lib.config_set(key, val)
     rng = np.random.default_rng(200 + k)
     for V in TOPK_V:
         if k > V:
@@ -274,12 +274,12 @@ def test_nonfinite_rows_flagged(cuda, lib):
     from paper_1805_02867_b200 import osmx
 
     rng = np.random.default_rng(5)
-    for shape in (0, 1, 2, 3):
+    for shape in (0, 1, 2, 3, 4):
         lib.config_set("shape", shape)
         lib.config_set("split_chunk", 2048 if shape == 3 else 0)
         for bad in (np.nan, np.inf, -np.inf):
             for V in (7, 3000, 40000):
-                if shape == 1 and V > 16384:
+                if shape in (1, 4) and V > 16384:
                     continue
                 x = rng.standard_normal((6, V)).astype(np.float32)
                 x[4, V // 2] = bad
@@ -310,3 +310,36 @@ def test_argument_errors(cuda, lib):
         osmx.softmax_topk(_dev(np.zeros((1, 100), np.float32)), 33)
     with pytest.raises(osmx.EmptyInputError):
         osmx.softmax(_dev(np.zeros((2, 0), np.float32)))
+
+
+@pytest.mark.parametrize("alg", ["online", "safe", "naive"])
+def test_softmax_staged_ring_wrap(cuda, oracle_mod, lib, alg):
+    """Enough rows per CTA that every slot of the staged ring is refilled
+    several times (D = 50 / 12 / 3 slots at V = 1000 / 4099 / 16384), with
+    rows of every 16-byte phase."""
+    from paper_1805_02867_b200 import osmx
+
+    lib.config_set("shape", SHAPES["staged"])
+    rng = np.random.default_rng(11)
+    for V, rows in ((1000, 148 * 60), (4099, 148 * 14), (16383, 148 * 5)):
+        x = rng.standard_normal((rows, V)).astype(np.float32)
+        y = osmx.softmax(_dev(x), alg=alg).cpu().numpy()
+        ref, st = oracle_mod.batch(f"{alg}_softmax", x)
+        assert (st == 0).all()
+        assert max_rel(y, ref) <= TOL, (alg, V)
+
+
+@pytest.mark.parametrize("variant", ["auto", "warp", "warp_u8", "warp_pf"])
+def test_online_fused_topk_many_rows(cuda, oracle_mod, lib, variant):
+    """Row counts around one wave of warps (the u8 heuristic's range)."""
+    from paper_1805_02867_b200 import osmx
+
+    for key, val in TOPK_VARIANTS[variant]:
+        lib.config_set(key, val)
+    rng = np.random.default_rng(12)
+    for rows, V in ((4000, 8192), (2000, 12289)):
+        x = dist("quantized2", rng, rows, V) if V == 8192 else dist("normal", rng, rows, V)
+        vals, idx = osmx.softmax_topk(_dev(x), 5, alg="online_fused")
+        rv, rz = _topk_ref(oracle_mod, "online_softmax_topk", x, 5)
+        assert np.array_equal(idx.cpu().numpy(), rz), (variant, rows, V)
+        assert max_rel(vals.cpu().numpy(), rv) <= TOL

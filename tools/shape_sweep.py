@@ -17,9 +17,10 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 
 import torch  # noqa: E402
 
-from bench import algo_bytes  # noqa: E402
+from bench import algo_bytes, n_rotating_sets, time_rotating  # noqa: E402
 from paper_1805_02867_b200 import _lib  # noqa: E402
 
+DEFAULTS = {"resident_max_v": 8192, "tma": 0, "topk_u8": -1}
 IDS = {"naive": 0, "safe": 1, "online": 2, "safe_unfused": 3, "safe_fused": 4, "online_fused": 5,
        "online_unfused": 6}
 
@@ -36,12 +37,13 @@ def main():
     lib = _lib.load()
     dev = torch.device("cuda", 0)
     sp = torch.cuda.current_stream().cuda_stream
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     knobs = [(kv.split("=")[0], [int(v) for v in kv.split("=")[1].split(",")]) for kv in a.knob] or [("shape", [0])]
     out = []
     for V in a.V:
-        x = torch.empty((a.rows, V), device=dev).normal_()
-        y = torch.empty_like(x)
+        nset = n_rotating_sets(8 * a.rows * V, l2, cap_bytes=24 << 30)
+        x = torch.empty((nset, a.rows, V), device=dev).normal_()
+        y = torch.empty_like(x) if any(IDS[n] < 3 for n in a.alg) else None
         vals = torch.empty((a.rows, a.k), device=dev)
         idx = torch.empty((a.rows, a.k), dtype=torch.int64, device=dev)
         for alg_name in a.alg:
@@ -53,25 +55,16 @@ def main():
                     nb = lib.osmx_workspace_bytes(alg, a.rows, V, a.k if topk else 0)
                     ws = torch.zeros(max(nb, 256), dtype=torch.uint8, device=dev)
 
-                    def fn():
+                    def launch(i, st):
                         if topk:
-                            return lib.osmx_softmax_topk(alg, x.data_ptr(), V, a.rows, V, a.k, vals.data_ptr(),
-                                                         idx.data_ptr(), ws.data_ptr(), ws.numel(), sp)
-                        return lib.osmx_softmax(alg, x.data_ptr(), V, y.data_ptr(), V, a.rows, V, ws.data_ptr(),
-                                                ws.numel(), sp)
+                            r = lib.osmx_softmax_topk(alg, x[i].data_ptr(), V, a.rows, V, a.k, vals.data_ptr(),
+                                                      idx.data_ptr(), ws.data_ptr(), ws.numel(), st)
+                        else:
+                            r = lib.osmx_softmax(alg, x[i].data_ptr(), V, y[i].data_ptr(), V, a.rows, V,
+                                                 ws.data_ptr(), ws.numel(), st)
+                        assert r == 0
 
-                    for _ in range(2):
-                        assert fn() == 0
-                    ts = []
-                    for _ in range(a.reps):
-                        flush.fill_(1)
-                        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                        e0.record()
-                        fn()
-                        e1.record()
-                        e1.synchronize()
-                        ts.append(e0.elapsed_time(e1))
-                    ms = statistics.median(ts)
+                    ms, ms_min = time_rotating(launch, nset, a.reps)
                     gbs = algo_bytes(alg_name, a.rows, V, a.k) / (ms * 1e-3) / 1e9
                     dram = (8 * a.rows * V if not topk else 4 * a.rows * V) / (ms * 1e-3) / 1e9
                     rec = {"V": V, "alg": alg_name, key: val, "ms": round(ms, 4), "GBps": round(gbs, 1),
@@ -79,7 +72,7 @@ def main():
                     out.append(rec)
                     print(json.dumps(rec), flush=True)
                     del ws
-                _lib.config_set(key, {"resident_max_v": 8192, "tma": 0}.get(key, 0))
+                _lib.config_set(key, DEFAULTS.get(key, 0))
         del x, y
     return out
 
