@@ -285,6 +285,15 @@ osmx_status osmx_config_set(const char* key, int64_t value) {
   } else if (!strcmp(key, "topk_threads")) {
     if (value != 0 && value != 32 && value != 128 && value != 256 && value != 512) return OSMX_ERR_INVALID_ARG;
     t.topk_threads = (int)value;
+  } else if (!strcmp(key, "staged_gw")) {
+    if (value != 0 && value != 1 && value != 2 && value != 4 && value != 8 && value != 16) return OSMX_ERR_INVALID_ARG;
+    t.staged_gw = (int)value;
+  } else if (!strcmp(key, "staged_ng")) {
+    if (value < 0 || value > 31) return OSMX_ERR_INVALID_ARG;
+    t.staged_ng = (int)value;
+  } else if (!strcmp(key, "staged_kb")) {
+    if (value != 0 && (value < 16 || value > 227)) return OSMX_ERR_INVALID_ARG;
+    t.staged_kb = (int)value;
   } else if (!strcmp(key, "topk_u8")) {
     if (value < -1 || value > 1) return OSMX_ERR_INVALID_ARG;
     t.topk_u8 = (int)value;
@@ -314,6 +323,9 @@ int64_t osmx_config_get(const char* key) {
   if (!strcmp(key, "tma")) return t.tma;
   if (!strcmp(key, "l2_prefetch")) return t.l2_prefetch;
   if (!strcmp(key, "topk_u8")) return t.topk_u8;
+  if (!strcmp(key, "staged_gw")) return t.staged_gw;
+  if (!strcmp(key, "staged_ng")) return t.staged_ng;
+  if (!strcmp(key, "staged_kb")) return t.staged_kb;
   if (!strcmp(key, "host_chunk_mb")) return g_host_chunk_mb;
   return -1;
 }

@@ -33,10 +33,13 @@ enum Shape : int {
 
 struct Tuning {
   int shape = kShapeAuto;       // force a family (0 = heuristic)
-  int resident_max_v = 8192;    // largest V held in registers (128-bit rows)
+  int resident_max_v = 2048;    // largest V held in registers (above: staged up to 16K)
   long long split_chunk = 0;    // elements per CTA in split mode (0 = auto)
   int stream_threads = 0;       // CTA size for stream kernels (0 = auto)
   int topk_threads = 0;         // CTA size for the fused top-K (0 = auto)
+  int staged_gw = 0;            // staged softmax: warps per row group (0 auto; 1,2,4,8,16)
+  int staged_ng = 0;            // staged softmax: row groups per CTA (0 auto; clamped to the slots)
+  int staged_kb = 0;            // staged softmax: ring (shared memory) per CTA, KB (0 auto)
   int topk_u8 = -1;             // warp-per-row top-K with 8 float4s in flight (-1 auto)
   int l2_prefetch = 0;          // bulk L2 prefetch distance in batches (0 = off)
   int tma = 0;                  // TMA-ring top-K: 0 off (default: the warp-per-row

@@ -25,7 +25,7 @@ bool softmax_uses_split(long long rows, long long V) {
   const auto& tn = tuning();
   if (tn.shape == kShapeSplit) return rows <= 65535;
   if (tn.shape != kShapeAuto) return false;
-  return V > resident_limit(false) && rows < 2LL * num_sms();
+  return V > std::max<long long>(resident_limit(false), kStagedMaxV) && rows < 2LL * num_sms();
 }
 
 cudaError_t launch_softmax(int alg, const float* x, long long ldx, float* y, long long ldy,

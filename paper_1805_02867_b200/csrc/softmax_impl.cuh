@@ -634,12 +634,15 @@ cudaError_t launch_alg(const float* x, long long ldx, float* y, long long ldy, l
                    ((reinterpret_cast<uintptr_t>(x) & 15u) == 0) && ((reinterpret_cast<uintptr_t>(y) & 15u) == 0);
   int shape = tn.shape;
   if (shape == osmx_host::kShapeAuto) {
-    // Measured on B200 (tools/shape_sweep.py, cold L2, 4000 rows): the
-    // register-resident rows win up to V = 8192 with 128-bit loads; rows that
-    // cannot use them (V % 4 != 0 / unaligned) only up to ~4096; beyond that
-    // the two-pass stream kernel (second pass from L2) is faster.
+    // Measured on B200 (tools/shape_sweep.py, inputs out of L2, 4000 and
+    // 32768 rows): register-resident rows win up to V ~ 1024; the TMA-staged
+    // shared-memory ring from there to 16K (1.1-1.5x the resident / stream
+    // kernels at V = 3K-10K); beyond, the stream kernel (one CTA per row) or
+    // the split kernel when there are too few rows to fill the SMs.
     if (V <= osmx_host::resident_limit(vec))
       shape = osmx_host::kShapeResident;
+    else if (V <= kStagedMaxV)
+      shape = osmx_host::kShapeStaged;
     else if (rows >= 2LL * osmx_host::num_sms())
       shape = osmx_host::kShapeStream;
     else

@@ -106,22 +106,26 @@ struct SOpSumD {
 __host__ __device__ inline int staged_slot_floats(long long V) { return (int)((V + 3 + 3) / 4 * 4); }
 
 // Shared-memory layout: [full D][empty D] mbarriers, group scratch, slots.
-__host__ __device__ inline size_t staged_scratch_off(int D) { return (size_t)16 * D; }
-template <int NG, int GW>
-__host__ __device__ inline size_t staged_slots_off(int D) {
-  return (staged_scratch_off(D) + (size_t)NG * 2 * GW * 8 + 127) / 128 * 128;
-}
+// Up to 64 slots and 31 consumer warps: a fixed 2 KB header.
+constexpr int kStagedMaxD = 64;
+__host__ __device__ inline size_t staged_scratch_off() { return (size_t)16 * kStagedMaxD; }
+__host__ __device__ inline size_t staged_slots_off() { return 2048; }
 
-template <int GW, int NG, int ALG>
-__global__ void __launch_bounds__(32 * (1 + GW * NG), 1)
+// NG (runtime) consumer groups of GW warps; blockDim = 32 * (1 + GW * NG).
+// Requires D >= NG: a group then never waits more than one phase ahead of a
+// slot's mbarrier (its previous row, loaded before this one, is >= D rows
+// back), so parity waits are unambiguous.
+template <int GW, int ALG>
+__global__ void __launch_bounds__(1024, 1)
     k_softmax_staged(const float* __restrict__ x, long long ldx, float* __restrict__ y, long long ldy,
                      long long rows, int V, int D, void* ws) {
   constexpr int GT = GW * 32;
+  const int NG = (blockDim.x / 32 - 1) / GW;
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + D;
   const int slotf = staged_slot_floats(V);
-  float* slots = reinterpret_cast<float*>(smem + staged_slots_off<NG, GW>(D));
+  float* slots = reinterpret_cast<float*>(smem + staged_slots_off());
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < D; ++s) {
@@ -163,7 +167,7 @@ __global__ void __launch_bounds__(32 * (1 + GW * NG), 1)
   const int lw = (w - 1) % GW;  // warp within the group
   const int tg = lw * 32 + lane;
   const int bar_id = 1 + g;
-  float* scr = reinterpret_cast<float*>(smem + staged_scratch_off(D)) + g * 4 * GW;  // 2*GW doubles
+  float* scr = reinterpret_cast<float*>(smem + staged_scratch_off()) + g * 4 * GW;  // 2*GW doubles
   double* scrd = reinterpret_cast<double*>(scr);
 
   long long j = g;
@@ -175,27 +179,26 @@ __global__ void __launch_bounds__(32 * (1 + GW * NG), 1)
     const int phase = (int)((reinterpret_cast<uintptr_t>(xr) >> 2) & 3);
     const int nq = (phase + V + 3) >> 2;
     const float4* sl4 = reinterpret_cast<const float4*>(slots + (size_t)s * slotf);
-    // element index of component 0 of slot float4 q is 4q - phase
-    auto masked = [&](int q) -> float4 {
+    // Slot float4 q holds elements 4q - phase .. 4q + 3 - phase.  Interior
+    // float4s [qa, qb) are entirely inside the row and need no masking; the
+    // <= 2 edge float4s (qe0 = 0 when phase > 0, qe1 = qb when the row ends
+    // mid-float4) are masked, one thread each.
+    const int qa = phase ? 1 : 0;
+    const int qb = (phase + V) >> 2 > qa ? (phase + V) >> 2 : qa;
+    const int qe0 = phase ? 0 : -1;
+    const int qe1 = (qb < nq && qb != qe0) ? qb : -1;
+    const int my_edge = tg == 0 ? qe0 : (tg == 1 ? qe1 : -1);
+    auto masked = [&](int q, float fill) -> float4 {
       float4 v = sl4[q];
       const int e0 = 4 * q - phase;
-      if (e0 < 0 || e0 + 4 > V) {
-        if (e0 + 0 < 0 || e0 + 0 >= V) v.x = kNegInf;
-        if (e0 + 1 < 0 || e0 + 1 >= V) v.y = kNegInf;
-        if (e0 + 2 < 0 || e0 + 2 >= V) v.z = kNegInf;
-        if (e0 + 3 < 0 || e0 + 3 >= V) v.w = kNegInf;
-      }
+      if (e0 + 0 < 0 || e0 + 0 >= V) v.x = fill;
+      if (e0 + 1 < 0 || e0 + 1 >= V) v.y = fill;
+      if (e0 + 2 < 0 || e0 + 2 >= V) v.z = fill;
+      if (e0 + 3 < 0 || e0 + 3 >= V) v.w = fill;
       return v;
     };
-    // min over the row's real elements (-inf detection); masked lanes -> +inf
-    auto vmin = [&](float4 v, int q) -> float {
-      const int e0 = 4 * q - phase;
-      float a = (e0 + 0 >= 0 && e0 + 0 < V) ? v.x : -kNegInf;
-      float b = (e0 + 1 >= 0 && e0 + 1 < V) ? v.y : -kNegInf;
-      float c = (e0 + 2 >= 0 && e0 + 2 < V) ? v.z : -kNegInf;
-      float d = (e0 + 3 >= 0 && e0 + 3 < V) ? v.w : -kNegInf;
-      return fminf(fminf(a, b), fminf(c, d));
-    };
+    auto min4 = [](float a, const float4& v) { return fminf(fminf(a, fminf(v.x, v.y)), fminf(v.z, v.w)); };
+    auto max4 = [](float a, const float4& v) { return fmaxf(fmaxf(a, fmaxf(v.x, v.y)), fmaxf(v.z, v.w)); };
 
     float M = 0.0f, r = 0.0f;
     double rd = 0.0;
@@ -205,23 +208,29 @@ __global__ void __launch_bounds__(32 * (1 + GW * NG), 1)
       // Alg. 3 lines 1-6: per thread, batch max first then one rescale.
       L2Acc acc;
       constexpr int U = 4;
-      int q = tg;
-      for (; q + (U - 1) * GT < nq; q += U * GT) {
+      int q = qa + tg;
+      for (; q + (U - 1) * GT < qb; q += U * GT) {
         float4 v[U];
         float bm = kNegInf;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          v[u] = masked(q + u * GT);
-          mn = fminf(mn, vmin(v[u], q + u * GT));
-          bm = fmaxf(bm, fmaxf(fmaxf(v[u].x, v[u].y), fmaxf(v[u].z, v[u].w)));
+          v[u] = sl4[q + u * GT];
+          mn = min4(mn, v[u]);
+          bm = max4(bm, v[u]);
         }
         acc.raise(bm);
-        if (bm != kNegInf) acc.add_batch<U>(v);
+        acc.add_batch<U>(v);
       }
-      for (; q < nq; q += GT) {
-        float4 v[1] = {masked(q)};
-        mn = fminf(mn, vmin(v[0], q));
-        const float bm = fmaxf(fmaxf(v[0].x, v[0].y), fmaxf(v[0].z, v[0].w));
+      for (; q < qb; q += GT) {
+        float4 v[1] = {sl4[q]};
+        mn = min4(mn, v[0]);
+        acc.raise(max4(kNegInf, v[0]));
+        acc.add_batch<1>(v);
+      }
+      if (my_edge >= 0) {
+        float4 v[1] = {masked(my_edge, kNegInf)};
+        mn = min4(mn, masked(my_edge, -kNegInf));
+        const float bm = max4(kNegInf, v[0]);
         acc.raise(bm);
         if (bm != kNegInf) acc.add_batch<1>(v);
       }
@@ -232,19 +241,31 @@ __global__ void __launch_bounds__(32 * (1 + GW * NG), 1)
       bad = !(tot.d == tot.d) || !isfinite(M) || mn == kNegInf;
     } else if constexpr (ALG == osmx_host::kSafe) {
       // kernels.hpp:54 max, :56 sum against it
-      float m = kNegInf;
-      for (int q = tg; q < nq; q += GT) {
-        const float4 v = masked(q);
-        mn = fminf(mn, vmin(v, q));
-        m = fmaxf(m, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
-        if (!(v.x == v.x && v.y == v.y && v.z == v.z && v.w == v.w)) mn = __int_as_float(0x7fffffff);
+      float m = kNegInf, chk = 0.0f;
+      for (int q = qa + tg; q < qb; q += GT) {
+        const float4 v = sl4[q];
+        mn = min4(mn, v);
+        m = max4(m, v);
+        chk = fmaf(v.x, 0.0f, fmaf(v.y, 0.0f, fmaf(v.z, 0.0f, fmaf(v.w, 0.0f, chk))));  // NaN iff inf/NaN
       }
+      if (my_edge >= 0) {
+        const float4 v = masked(my_edge, kNegInf);
+        m = max4(m, v);
+        mn = min4(mn, masked(my_edge, -kNegInf));
+        const float4 z = masked(my_edge, 0.0f);  // out-of-row lanes must not poison chk
+        chk = fmaf(z.x, 0.0f, fmaf(z.y, 0.0f, fmaf(z.z, 0.0f, fmaf(z.w, 0.0f, chk))));
+      }
+      if (!(chk == chk)) mn = kNegInf;  // -inf survives the fminf group reduce (NaN would not)
       M = SGrp<GW>::red(m, SOpMax(), scr, bar_id, lw);
       mn = SGrp<GW>::red(mn, SOpMin(), scr, bar_id, lw);
       L2Acc sacc;
       sacc.raise(M);
-      for (int q = tg; q < nq; q += GT) {
-        float4 v[1] = {masked(q)};
+      for (int q = qa + tg; q < qb; q += GT) {
+        float4 v[1] = {sl4[q]};
+        sacc.add_batch<1>(v);
+      }
+      if (my_edge >= 0) {
+        float4 v[1] = {masked(my_edge, kNegInf)};
         sacc.add_batch<1>(v);
       }
       float d = (M == kNegInf) ? 0.0f : sacc.finish().d;
@@ -255,10 +276,16 @@ __global__ void __launch_bounds__(32 * (1 + GW * NG), 1)
       // naive: d = sum double(expf(x)) (kernels.hpp:43-44), no max shift
       double d = 0.0;
       float mx = kNegInf;
-      for (int q = tg; q < nq; q += GT) {
-        const float4 v = masked(q);
-        mn = fminf(mn, vmin(v, q));
-        mx = fmaxf(mx, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
+      for (int q = qa + tg; q < qb; q += GT) {
+        const float4 v = sl4[q];
+        mn = min4(mn, v);
+        mx = max4(mx, v);
+        d += ((double)expf(v.x) + (double)expf(v.y)) + ((double)expf(v.z) + (double)expf(v.w));
+      }
+      if (my_edge >= 0) {
+        const float4 v = masked(my_edge, kNegInf);  // expf(-inf) = 0
+        mn = min4(mn, masked(my_edge, -kNegInf));
+        mx = max4(mx, v);
         d += ((double)expf(v.x) + (double)expf(v.y)) + ((double)expf(v.z) + (double)expf(v.w));
       }
       d = SGrp<GW>::red(d, SOpSumD(), scrd, bar_id, lw);
@@ -278,18 +305,38 @@ __global__ void __launch_bounds__(32 * (1 + GW * NG), 1)
     };
     const bool same_phase = ((reinterpret_cast<uintptr_t>(yr) >> 2) & 3) == (uintptr_t)phase;
     float* yb = yr - phase;  // yb[4q + c] <-> slot float4 q component c
-    for (int q = tg; q < nq; q += GT) {
-      const float4 v = sl4[q];
-      const float4 o = make_float4(f(v.x), f(v.y), f(v.z), f(v.w));
-      const int e0 = 4 * q - phase;
-      if (same_phase && e0 >= 0 && e0 + 4 <= V) {
-        st_f4(yb + 4 * q, o);
-      } else {
-        if (e0 + 0 >= 0 && e0 + 0 < V) st_f1(yr + e0 + 0, o.x);
-        if (e0 + 1 >= 0 && e0 + 1 < V) st_f1(yr + e0 + 1, o.y);
-        if (e0 + 2 >= 0 && e0 + 2 < V) st_f1(yr + e0 + 2, o.z);
-        if (e0 + 3 >= 0 && e0 + 3 < V) st_f1(yr + e0 + 3, o.w);
+    if (same_phase) {
+      constexpr int U2 = 4;
+      int q = qa + tg;
+      for (; q + (U2 - 1) * GT < qb; q += U2 * GT) {
+        float4 v[U2];
+#pragma unroll
+        for (int u = 0; u < U2; ++u) v[u] = sl4[q + u * GT];
+#pragma unroll
+        for (int u = 0; u < U2; ++u)
+          st_f4(yb + 4 * (q + u * GT), make_float4(f(v[u].x), f(v[u].y), f(v[u].z), f(v[u].w)));
       }
+      for (; q < qb; q += GT) {
+        const float4 v = sl4[q];
+        st_f4(yb + 4 * q, make_float4(f(v.x), f(v.y), f(v.z), f(v.w)));
+      }
+    } else {
+      for (int q = qa + tg; q < qb; q += GT) {
+        const float4 v = sl4[q];
+        float* d = yb + 4 * q;
+        st_f1(d + 0, f(v.x));
+        st_f1(d + 1, f(v.y));
+        st_f1(d + 2, f(v.z));
+        st_f1(d + 3, f(v.w));
+      }
+    }
+    if (my_edge >= 0) {
+      const float4 v = sl4[my_edge];
+      const int e0 = 4 * my_edge - phase;
+      if (e0 + 0 >= 0 && e0 + 0 < V) st_f1(yr + e0 + 0, f(v.x));
+      if (e0 + 1 >= 0 && e0 + 1 < V) st_f1(yr + e0 + 1, f(v.y));
+      if (e0 + 2 >= 0 && e0 + 2 < V) st_f1(yr + e0 + 2, f(v.z));
+      if (e0 + 3 >= 0 && e0 + 3 < V) st_f1(yr + e0 + 3, f(v.w));
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
@@ -297,25 +344,30 @@ __global__ void __launch_bounds__(32 * (1 + GW * NG), 1)
 }
 
 // Largest dynamic shared memory the staged kernels use per CTA.
-constexpr int kStagedSmem = 200 * 1024;
+constexpr int kStagedSmemMax = 227 * 1024;
 
-template <int GW, int NG, int ALG>
+template <int GW, int ALG>
 cudaError_t run_staged_cfg(const float* x, long long ldx, float* y, long long ldy, long long rows, long long V,
-                           void* ws, cudaStream_t st) {
+                           void* ws, cudaStream_t st, int ng, int ring_kb) {
+  const auto& tn = osmx_host::tuning();
+  if (tn.staged_kb > 0) ring_kb = tn.staged_kb;
+  if (tn.staged_ng > 0) ng = tn.staged_ng;
   const size_t slot = (size_t)staged_slot_floats(V) * 4;
-  int D = (int)((kStagedSmem - 1024) / slot);
-  D = D > 64 ? 64 : D;
-  if (D < NG) return cudaErrorInvalidValue;
-  const size_t smem = staged_slots_off<NG, GW>(D) + (size_t)D * slot;
+  const size_t ring = std::min<size_t>((size_t)ring_kb * 1024, kStagedSmemMax) - staged_slots_off();
+  int D = (int)std::min<size_t>(ring / slot, kStagedMaxD);
+  ng = std::min(ng, std::min(D, 31 / GW));
+  if (ng < 1) return cudaErrorInvalidValue;
+  const int ctas_per_sm = std::max(1, (228 * 1024) / (ring_kb * 1024 + 1024));
+  const size_t smem = staged_slots_off() + (size_t)D * slot;
   static bool attr_set = false;  // per instantiation; the attribute is per function
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_softmax_staged<GW, NG, ALG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         kStagedSmem);
+    cudaError_t e = cudaFuncSetAttribute(k_softmax_staged<GW, ALG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kStagedSmemMax);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  const long long grid = std::min<long long>(rows, (long long)osmx_host::num_sms());
-  k_softmax_staged<GW, NG, ALG><<<(unsigned)grid, 32 * (1 + GW * NG), smem, st>>>(x, ldx, y, ldy, rows, (int)V, D, ws);
+  const long long grid = std::min<long long>(rows, (long long)osmx_host::num_sms() * ctas_per_sm);
+  k_softmax_staged<GW, ALG><<<(unsigned)grid, 32 * (1 + GW * ng), smem, st>>>(x, ldx, y, ldy, rows, (int)V, D, ws);
   osmx_host::count_launch();
   return cudaGetLastError();
 }
@@ -326,10 +378,27 @@ constexpr long long kStagedMaxV = 16384;
 template <int ALG>
 cudaError_t run_staged(const float* x, long long ldx, float* y, long long ldy, long long rows, long long V,
                        void* ws, cudaStream_t st) {
-  if (V <= 1024) return run_staged_cfg<1, 16, ALG>(x, ldx, y, ldy, rows, V, ws, st);
-  if (V <= 4096) return run_staged_cfg<2, 8, ALG>(x, ldx, y, ldy, rows, V, ws, st);
-  if (V <= 8192) return run_staged_cfg<4, 4, ALG>(x, ldx, y, ldy, rows, V, ws, st);
-  return run_staged_cfg<8, 2, ALG>(x, ldx, y, ldy, rows, V, ws, st);
+  // Group width (warps per row) and group count per V, from
+  // tools/shape_sweep.py on B200 (4000 and 32768 rows, gw x ng grid,
+  // profiles/r01s2_staged_sweep.md): 2-warp groups x 6 up to V = 4096,
+  // 4-warp groups x 6 up to 8192, x 3 above; at least one slot stays in
+  // flight (ng <= D - 1), which matters once only 3-5 rows fit the ring.
+  int gw = osmx_host::tuning().staged_gw;
+  const int kb = 220;
+  if (gw == 0) gw = V <= 1024 ? 1 : V <= 4096 ? 2 : 4;
+  int ng = gw == 1 ? 16 : V <= 8192 ? 6 : 3;
+  {
+    const size_t slot = (size_t)staged_slot_floats(V) * 4;
+    const int D = (int)std::min<size_t>((size_t)(kb * 1024 - staged_slots_off()) / slot, kStagedMaxD);
+    if (D >= 2) ng = std::min(ng, D - 1);
+  }
+  switch (gw) {
+    case 1: return run_staged_cfg<1, ALG>(x, ldx, y, ldy, rows, V, ws, st, ng, kb);
+    case 2: return run_staged_cfg<2, ALG>(x, ldx, y, ldy, rows, V, ws, st, ng, kb);
+    case 4: return run_staged_cfg<4, ALG>(x, ldx, y, ldy, rows, V, ws, st, ng, kb);
+    case 8: return run_staged_cfg<8, ALG>(x, ldx, y, ldy, rows, V, ws, st, ng, kb);
+    default: return run_staged_cfg<16, ALG>(x, ldx, y, ldy, rows, V, ws, st, ng, kb);
+  }
 }
 
 }  // namespace

@@ -20,7 +20,7 @@ import torch  # noqa: E402
 from bench import algo_bytes, n_rotating_sets, time_rotating  # noqa: E402
 from paper_1805_02867_b200 import _lib  # noqa: E402
 
-DEFAULTS = {"resident_max_v": 8192, "tma": 0, "topk_u8": -1}
+DEFAULTS = {"resident_max_v": 2048, "tma": 0, "topk_u8": -1, "staged_kb": 0, "staged_gw": 0, "staged_ng": 0}
 IDS = {"naive": 0, "safe": 1, "online": 2, "safe_unfused": 3, "safe_fused": 4, "online_fused": 5,
        "online_unfused": 6}
 
@@ -33,8 +33,11 @@ def main():
     ap.add_argument("--k", type=int, default=5)
     ap.add_argument("--reps", type=int, default=9)
     ap.add_argument("--knob", action="append", default=[], help="key=v1,v2,...")
+    ap.add_argument("--set", action="append", default=[], help="key=v fixed for the whole run")
     a = ap.parse_args()
     lib = _lib.load()
+    for kv in a.set:
+        _lib.config_set(kv.split("=")[0], int(kv.split("=")[1]))
     dev = torch.device("cuda", 0)
     sp = torch.cuda.current_stream().cuda_stream
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
