@@ -271,7 +271,7 @@ osmx_status osmx_config_set(const char* key, int64_t value) {
   if (!key) return OSMX_ERR_INVALID_ARG;
   auto& t = tuning();
   if (!strcmp(key, "shape")) {
-    if (value < 0 || value > 4) return OSMX_ERR_INVALID_ARG;
+    if (value < 0 || value > 5) return OSMX_ERR_INVALID_ARG;
     t.shape = (int)value;
   } else if (!strcmp(key, "resident_max_v")) {
     if (value < 0 || value > 16384) return OSMX_ERR_INVALID_ARG;
@@ -282,9 +282,15 @@ osmx_status osmx_config_set(const char* key, int64_t value) {
   } else if (!strcmp(key, "stream_threads")) {
     if (value != 0 && value != 256 && value != 512 && value != 1024) return OSMX_ERR_INVALID_ARG;
     t.stream_threads = (int)value;
+  } else if (!strcmp(key, "stream_ctas")) {
+    if (value < 0 || value > 32) return OSMX_ERR_INVALID_ARG;
+    t.stream_ctas = (int)value;
   } else if (!strcmp(key, "topk_threads")) {
     if (value != 0 && value != 32 && value != 128 && value != 256 && value != 512) return OSMX_ERR_INVALID_ARG;
     t.topk_threads = (int)value;
+  } else if (!strcmp(key, "cluster_size")) {
+    if (value < 0 || value > 16) return OSMX_ERR_INVALID_ARG;
+    t.cluster_size = (int)value;
   } else if (!strcmp(key, "staged_gw")) {
     if (value != 0 && value != 1 && value != 2 && value != 4 && value != 8 && value != 16) return OSMX_ERR_INVALID_ARG;
     t.staged_gw = (int)value;
@@ -294,6 +300,9 @@ osmx_status osmx_config_set(const char* key, int64_t value) {
   } else if (!strcmp(key, "staged_kb")) {
     if (value != 0 && (value < 16 || value > 227)) return OSMX_ERR_INVALID_ARG;
     t.staged_kb = (int)value;
+  } else if (!strcmp(key, "topk_pipe")) {
+    if (value < 0 || value > 3) return OSMX_ERR_INVALID_ARG;
+    t.topk_pipe = (int)value;
   } else if (!strcmp(key, "topk_u8")) {
     if (value < -1 || value > 1) return OSMX_ERR_INVALID_ARG;
     t.topk_u8 = (int)value;
@@ -323,7 +332,10 @@ int64_t osmx_config_get(const char* key) {
   if (!strcmp(key, "tma")) return t.tma;
   if (!strcmp(key, "l2_prefetch")) return t.l2_prefetch;
   if (!strcmp(key, "topk_u8")) return t.topk_u8;
+  if (!strcmp(key, "topk_pipe")) return t.topk_pipe;
+  if (!strcmp(key, "stream_ctas")) return t.stream_ctas;
   if (!strcmp(key, "staged_gw")) return t.staged_gw;
+  if (!strcmp(key, "cluster_size")) return t.cluster_size;
   if (!strcmp(key, "staged_ng")) return t.staged_ng;
   if (!strcmp(key, "staged_kb")) return t.staged_kb;
   if (!strcmp(key, "host_chunk_mb")) return g_host_chunk_mb;

@@ -54,6 +54,27 @@ __device__ __forceinline__ float ld_f1_last(const float* p) {
                : "l"(p), "l"(pol_evict_first()));
   return r;
 }
+// First read of data the same CTA reads again soon (two-pass kernels with a
+// bounded in-flight footprint): evict-last L2 policy.
+__device__ __forceinline__ unsigned long long pol_evict_last() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ float4 ld_f4_keep(const float* p) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p), "l"(pol_evict_last()));
+  return r;
+}
+__device__ __forceinline__ float ld_f1_keep(const float* p) {
+  float r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;"
+               : "=f"(r)
+               : "l"(p), "l"(pol_evict_last()));
+  return r;
+}
 // Output is never re-read by the kernel: streaming (evict-first) stores.
 __device__ __forceinline__ void st_f4(float* p, float4 v) {
   asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),

@@ -29,6 +29,7 @@ enum Shape : int {
   kShapeStream = 2,    // one CTA per row, every pass streams global memory
   kShapeSplit = 3,     // row split over S CTAs, (m,d)/top-K records + combine
   kShapeStaged = 4,    // rows staged in a TMA-fed shared-memory ring (persistent)
+  kShapeCluster = 5,   // row slices staged across a thread-block cluster (DSMEM merge)
 };
 
 struct Tuning {
@@ -36,10 +37,13 @@ struct Tuning {
   int resident_max_v = 2048;    // largest V held in registers (above: staged up to 16K)
   long long split_chunk = 0;    // elements per CTA in split mode (0 = auto)
   int stream_threads = 0;       // CTA size for stream kernels (0 = auto)
+  int stream_ctas = 0;          // stream softmax: persistent CTAs per SM + evict-last pass 1 (0 = off)
   int topk_threads = 0;         // CTA size for the fused top-K (0 = auto)
+  int cluster_size = 0;         // cluster softmax: CTAs per row (0 auto; 1..16)
   int staged_gw = 0;            // staged softmax: warps per row group (0 auto; 1,2,4,8,16)
   int staged_ng = 0;            // staged softmax: row groups per CTA (0 auto; clamped to the slots)
   int staged_kb = 0;            // staged softmax: ring (shared memory) per CTA, KB (0 auto)
+  int topk_pipe = 0;            // warp-per-row top-K via a cp.async smem pipeline (0 off; 1..3 layouts)
   int topk_u8 = -1;             // warp-per-row top-K with 8 float4s in flight (-1 auto)
   int l2_prefetch = 0;          // bulk L2 prefetch distance in batches (0 = off)
   int tma = 0;                  // TMA-ring top-K: 0 off (default: the warp-per-row

@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(TPR > 256 ? TPR : 256)
 
 // --------------------------------------------------------------- stream --
 // One CTA per row; every pass of the algorithm reads global memory.
-template <int BLOCK, int U, int ALG>
+template <int BLOCK, int U, int ALG, int P1 = 0>
 __global__ void __launch_bounds__(BLOCK)
     k_softmax_stream(const float* __restrict__ x, long long ldx, float* __restrict__ y,
                      long long ldy, long long rows, long long V, void* ws, int pf) {
@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(BLOCK)
     if constexpr (ALG == osmx_host::kOnline) {
       // Pass 1: Alg. 3 lines 1-6, batch-max-first update per U float4s.
       L2Acc acc;
-      stream_seg<BLOCK, U, false>(
+      stream_seg<BLOCK, U, P1>(
           s, t,
           [&](float v, long long) {
             mn = fminf(mn, v);
@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(BLOCK)
     } else if constexpr (ALG == osmx_host::kSafe) {
       // Pass 1: max (kernels.hpp:54).  Pass 2: normalizer (:56).
       float m = kNegInf;
-      stream_seg<BLOCK, U, false>(
+      stream_seg<BLOCK, U, P1>(
           s, t,
           [&](float v, long long) {
             m = fmaxf(m, v);
@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(BLOCK)
       mn = cta_min<NW>(mn, smf);
       L2Acc sacc;  // sum e^(x - M) as one FFMA + ex2 per element
       sacc.raise(M);
-      stream_seg<BLOCK, U, false>(
+      stream_seg<BLOCK, U, P1>(
           s, t, [&](float v, long long) { sacc.d += sacc.term(v); },
           [&](float4 (&v)[U], long long, int) { sacc.add_batch<U>(v); });
       float d = (M == kNegInf) ? 0.0f : sacc.finish().d;
@@ -293,7 +293,7 @@ __global__ void __launch_bounds__(BLOCK)
       // Naive: d = sum double(expf(x)) (kernels.hpp:43-44).
       double d = 0.0;
       float mx = kNegInf;
-      stream_seg<BLOCK, U, false>(
+      stream_seg<BLOCK, U, P1>(
           s, t,
           [&](float v, long long) {
             d += (double)expf(v);
@@ -581,6 +581,18 @@ cudaError_t run_stream(const float* x, long long ldx, float* y, long long ldy, l
   int threads = osmx_host::tuning().stream_threads;
   const int pf = osmx_host::tuning().l2_prefetch;
   if (threads == 0) threads = V >= 65536 ? 512 : 256;
+  const int keep = osmx_host::tuning().stream_ctas;  // > 0: persistent, CTAs per SM, evict-last pass 1
+  if (keep > 0) {
+    const long long grid = std::min<long long>(rows, (long long)keep * osmx_host::num_sms());
+    if (threads == 1024)
+      k_softmax_stream<1024, 4, ALG, 2><<<(unsigned)grid, 1024, 0, st>>>(x, ldx, y, ldy, rows, V, ws, pf);
+    else if (threads == 512)
+      k_softmax_stream<512, 4, ALG, 2><<<(unsigned)grid, 512, 0, st>>>(x, ldx, y, ldy, rows, V, ws, pf);
+    else
+      k_softmax_stream<256, 4, ALG, 2><<<(unsigned)grid, 256, 0, st>>>(x, ldx, y, ldy, rows, V, ws, pf);
+    osmx_host::count_launch();
+    return cudaGetLastError();
+  }
   const long long grid = std::min<long long>(rows, 1LL << 30);
   if (threads == 1024)
     k_softmax_stream<1024, 4, ALG><<<(unsigned)grid, 1024, 0, st>>>(x, ldx, y, ldy, rows, V, ws, pf);
@@ -643,14 +655,16 @@ cudaError_t launch_alg(const float* x, long long ldx, float* y, long long ldy, l
       shape = osmx_host::kShapeResident;
     else if (V <= kStagedMaxV)
       shape = osmx_host::kShapeStaged;
+    else if (V <= kClusterMaxV && rows >= osmx_host::num_sms() / 2)
+      shape = osmx_host::kShapeCluster;
     else if (rows >= 2LL * osmx_host::num_sms())
       shape = osmx_host::kShapeStream;
     else
       shape = osmx_host::kShapeSplit;
   }
   if (shape == osmx_host::kShapeResident && V > 16384) shape = osmx_host::kShapeStream;
-  if (shape == osmx_host::kShapeStaged) {
-    if (V <= kStagedMaxV) return run_staged<ALG>(x, ldx, y, ldy, rows, V, ws, st);
+  if (shape == osmx_host::kShapeStaged || shape == osmx_host::kShapeCluster) {
+    if (V <= kClusterMaxV || osmx_host::tuning().cluster_size > 0) return run_staged<ALG>(x, ldx, y, ldy, rows, V, ws, st);
     shape = osmx_host::kShapeStream;
   }
   if (shape == osmx_host::kShapeSplit && rows > 65535) shape = osmx_host::kShapeStream;

@@ -1,31 +1,40 @@
 // softmax_staged.cuh -- TMA-staged, shared-memory-resident batched softmax
-// (naive / safe / online) for rows that fit in shared memory.
+// (naive / safe / online): every element crosses HBM exactly twice (one
+// read, one write), both streams overlapped across rows.
 //
-// Same algorithms as softmax_impl.cuh (reference kernels.hpp:39-69), but
-// each row crosses HBM exactly twice (one read, one write) with both streams
-// overlapped across rows:
+// Same algorithms as softmax_impl.cuh (reference kernels.hpp:39-69).  A row
+// is owned by a thread-block cluster of C CTAs (C = 1 for V <= 16K; up to 16
+// for longer rows): CTA c of the cluster holds slice [c*Sv, (c+1)*Sv) of it
+// (Sv a multiple of 4, so every slice keeps the row's 16-byte phase).
 //
-//   warp 0        producer: lane 0 copies whole rows into a D-slot
-//                 shared-memory ring -- the 16-byte aligned body with one
-//                 1-D bulk copy (cp.async.bulk, UBLKCP), the <= 3 + 3 head /
-//                 tail elements with 4-byte cp.async -- completing on the
-//                 slot's "full" mbarrier.  It runs up to D rows ahead.
-//   warps 1..     NG consumer groups of GW warps; group g takes the CTA's
-//                 rows g, g+NG, ...: every pass of the algorithm (online:
-//                 (m, d) then scale; safe: max, sum, scale) reads the slot
-//                 with LDS.128, the group merges with shuffles (+ a named
-//                 barrier when GW > 1), and the scale pass stores y straight
-//                 to global memory with 128-bit streaming stores.  The group
-//                 then releases the slot ("empty" mbarrier).
+//   warp 0        producer: lane 0 copies the CTA's slice of each row into a
+//                 D-slot shared-memory ring -- the 16-byte aligned body with
+//                 one 1-D bulk copy (cp.async.bulk, UBLKCP), the <= 3 + 3
+//                 edge elements with 4-byte cp.async -- completing on the
+//                 slot's "full" mbarrier; it runs up to D rows ahead.
+//   warps 1..     NG consumer groups of GW warps; group g takes the rows
+//                 g, g+NG, ... of its cluster.  Every pass of the algorithm
+//                 (online: (m, d) then scale; safe: max, sum, scale; naive:
+//                 sum, scale) reads the slot with LDS.128; the group merges
+//                 with shuffles (+ a named barrier when GW > 1).  With C > 1
+//                 the group's 16-byte record goes to group g of every CTA of
+//                 the cluster by st.async (distributed shared memory,
+//                 completing on that CTA's record mbarrier -- no fence), and
+//                 each CTA merges the C records in rank order, the
+//                 reference's contiguous-chunk merge (normalizer.hpp:73-85);
+//                 safe exchanges twice (max, then the sum against it).  The
+//                 scale pass stores y straight to global memory with 128-bit
+//                 streaming stores, then the group releases the slot.
 //
-// Row r is placed in its slot at float offset phase(r) = (address / 4) % 4,
-// so slot float4 q holds row elements 4q - phase .. 4q + 3 - phase: every
-// float4 of the slot is aligned both in shared memory and -- when y rows
-// have x's alignment phase -- in global memory, and rows of any V or ld
-// keep 128-bit accesses.  Out-of-row lanes of the first / last float4 are
-// masked (-inf for reductions, not stored).
+// Slot layout: the slice is placed at float offset phase = (address/4) % 4,
+// so slot float4 q holds slice elements 4q - phase .. 4q + 3 - phase; every
+// interior float4 is aligned in shared and (when y has x's phase) global
+// memory, whatever V and ld are.  The <= 2 edge float4s are masked.
 //
-// Persistent: one CTA per SM, rows grid-strided; D * slot <= ~200 KB.
+// Ordering: D >= NG + 1 so a group never waits more than one phase ahead of
+// a slot mbarrier; records are double-buffered per group by row parity --
+// a peer writes a group's (k+2)-th record only after it has received this
+// CTA's (k+1)-th, which this CTA sends after reading its k-th records.
 #pragma once
 
 #include "common.cuh"
@@ -105,36 +114,92 @@ struct SOpSumD {
 
 __host__ __device__ inline int staged_slot_floats(long long V) { return (int)((V + 3 + 3) / 4 * 4); }
 
-// Shared-memory layout: [full D][empty D] mbarriers, group scratch, slots.
-// Up to 64 slots and 31 consumer warps: a fixed 2 KB header.
+struct SRecX {  // one slice's contribution, exchanged across the cluster (16 B)
+  float m;      // max / running max
+  float mn;     // min (-inf marks a non-finite element)
+  double d;     // normalizer (naive: sum e^x; online: relative to m; safe round 1: relative to M)
+};
+
+__device__ __forceinline__ unsigned cl_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned cl_size() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned cl_id() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned cl_count() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cl_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// Asynchronous store of a record into CTA `rank`'s copy of `local`,
+// completing 16 transaction bytes on that CTA's copy of `bar`.
+__device__ __forceinline__ void st_async_rec(SRecX* local, uint64_t* bar, unsigned rank, const SRecX& r) {
+  uint32_t ra, rb;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(local)), "r"(rank));
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(smem_u32(bar)), "r"(rank));
+  const unsigned long long db = (unsigned long long)__double_as_longlong(r.d);
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(ra),
+               "r"(__float_as_uint(r.m)), "r"(__float_as_uint(r.mn)), "r"((unsigned)(db & 0xffffffffu)),
+               "r"((unsigned)(db >> 32)), "r"(rb)
+               : "memory");
+}
+
+// Shared-memory layout (bytes):
+//   0      full[64], empty[64] slot mbarriers
+//   1024   record mbarriers [group][round][parity] (<= 31 groups)
+//   2048   group reduce scratch (4 * GW floats per group)
+//   2560   records [group][round][parity][C] (C > 1 only)
+//   ...    slots (128-byte aligned)
 constexpr int kStagedMaxD = 64;
-__host__ __device__ inline size_t staged_scratch_off() { return (size_t)16 * kStagedMaxD; }
-__host__ __device__ inline size_t staged_slots_off() { return 2048; }
+__host__ __device__ inline size_t staged_recbar_off() { return 1024; }
+__host__ __device__ inline size_t staged_scratch_off() { return 2048; }
+__host__ __device__ inline size_t staged_recs_off() { return 2560; }
+__host__ __device__ inline size_t staged_slots_off(int ng, int C) {
+  const size_t recs = C > 1 ? (size_t)ng * 4 * C * sizeof(SRecX) : 0;
+  return (staged_recs_off() + recs + 127) / 128 * 128;
+}
 
 // NG (runtime) consumer groups of GW warps; blockDim = 32 * (1 + GW * NG).
-// Requires D >= NG: a group then never waits more than one phase ahead of a
-// slot's mbarrier (its previous row, loaded before this one, is >= D rows
-// back), so parity waits are unambiguous.
 template <int GW, int ALG>
 __global__ void __launch_bounds__(1024, 1)
     k_softmax_staged(const float* __restrict__ x, long long ldx, float* __restrict__ y, long long ldy,
-                     long long rows, int V, int D, void* ws) {
+                     long long rows, int V, int Sv, int D, void* ws) {
   constexpr int GT = GW * 32;
   const int NG = (blockDim.x / 32 - 1) / GW;
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
-  uint64_t* empty = full + D;
-  const int slotf = staged_slot_floats(V);
-  float* slots = reinterpret_cast<float*>(smem + staged_slots_off());
+  uint64_t* empty = full + kStagedMaxD;
+  uint64_t* recbar = reinterpret_cast<uint64_t*>(smem + staged_recbar_off());
+  SRecX* recs = reinterpret_cast<SRecX*>(smem + staged_recs_off());
+  const unsigned C = cl_size(), c = cl_rank();
+  const long long ncl = cl_count(), cl = cl_id();
+  const int slotf = staged_slot_floats(Sv);
+  float* slots = reinterpret_cast<float*>(smem + staged_slots_off(NG, (int)C));
+  const int s0 = (int)c * Sv;                                  // slice start (multiple of 4)
+  const int n = V - s0 <= 0 ? 0 : (V - s0 < Sv ? V - s0 : Sv);  // slice length (may be 0)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < D; ++s) {
       mbar_init(&full[s], 2);    // expect_tx arrival + cp.async arrival
       mbar_init(&empty[s], GW);  // one arrival per consumer warp of the group
     }
+    for (int b = 0; b < 4 * NG; ++b) mbar_init(&recbar[b], 1);  // local expect_tx; C x 16 B of st.async
     fence_mbar_init();
   }
   __syncthreads();
+  if (C > 1) cl_sync();  // peers' barriers exist before any st.async reaches them
 
   const int w = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -142,262 +207,341 @@ __global__ void __launch_bounds__(1024, 1)
     // ------------------------------------------------------------ producer
     if (lane == 0) {
       long long j = 0;
-      for (long long row = blockIdx.x; row < rows; row += gridDim.x, ++j) {
+      for (long long row = cl; row < rows; row += ncl, ++j) {
         const int s = (int)(j % D);
         if (j >= D) mbar_wait(&empty[s], (uint32_t)(((j / D) - 1) & 1));
-        const float* xr = x + row * ldx;
-        const int phase = (int)((reinterpret_cast<uintptr_t>(xr) >> 2) & 3);
+        const float* xs = x + row * ldx + s0;
+        const int phase = (int)((reinterpret_cast<uintptr_t>(xs) >> 2) & 3);
         int head = phase ? 4 - phase : 0;
-        if (head > V) head = V;
-        const int nvec = (V - head) >> 2;
-        const int tail = V - head - 4 * nvec;
-        float* sl = slots + (size_t)s * slotf + phase;  // sl[e] <- xr[e]
-        for (int e = 0; e < head; ++e) cp_async_4(sl + e, xr + e);
-        for (int e = V - tail; e < V; ++e) cp_async_4(sl + e, xr + e);
+        if (head > n) head = n;
+        const int nvec = (n - head) >> 2;
+        const int tail = n - head - 4 * nvec;
+        float* sl = slots + (size_t)s * slotf + phase;  // sl[e] <- xs[e]
+        for (int e = 0; e < head; ++e) cp_async_4(sl + e, xs + e);
+        for (int e = n - tail; e < n; ++e) cp_async_4(sl + e, xs + e);
         cp_async_mbar_arrive(&full[s]);
         mbar_arrive_expect_tx(&full[s], (uint32_t)nvec * 16u);
-        if (nvec > 0) tma_load_1d_nohint(sl + head, xr + head, (uint32_t)nvec * 16u, &full[s]);
+        if (nvec > 0) tma_load_1d_nohint(sl + head, xs + head, (uint32_t)nvec * 16u, &full[s]);
       }
     }
-    return;
-  }
+  } else {
+    // ------------------------------------------------------------ consumers
+    const int g = (w - 1) / GW;   // group
+    const int lw = (w - 1) % GW;  // warp within the group
+    const int tg = lw * 32 + lane;
+    const int bar_id = 1 + g;
+    float* scr = reinterpret_cast<float*>(smem + staged_scratch_off()) + g * 4 * GW;  // 2*GW doubles
+    double* scrd = reinterpret_cast<double*>(scr);
 
-  // -------------------------------------------------------------- consumers
-  const int g = (w - 1) / GW;   // group
-  const int lw = (w - 1) % GW;  // warp within the group
-  const int tg = lw * 32 + lane;
-  const int bar_id = 1 + g;
-  float* scr = reinterpret_cast<float*>(smem + staged_scratch_off()) + g * 4 * GW;  // 2*GW doubles
-  double* scrd = reinterpret_cast<double*>(scr);
-
-  long long j = g;
-  for (long long row = blockIdx.x + (long long)g * gridDim.x; row < rows; row += (long long)NG * gridDim.x, j += NG) {
-    const int s = (int)(j % D);
-    mbar_wait(&full[s], (uint32_t)((j / D) & 1));
-    const float* xr = x + row * ldx;
-    float* yr = y + row * ldy;
-    const int phase = (int)((reinterpret_cast<uintptr_t>(xr) >> 2) & 3);
-    const int nq = (phase + V + 3) >> 2;
-    const float4* sl4 = reinterpret_cast<const float4*>(slots + (size_t)s * slotf);
-    // Slot float4 q holds elements 4q - phase .. 4q + 3 - phase.  Interior
-    // float4s [qa, qb) are entirely inside the row and need no masking; the
-    // <= 2 edge float4s (qe0 = 0 when phase > 0, qe1 = qb when the row ends
-    // mid-float4) are masked, one thread each.
-    const int qa = phase ? 1 : 0;
-    const int qb = (phase + V) >> 2 > qa ? (phase + V) >> 2 : qa;
-    const int qe0 = phase ? 0 : -1;
-    const int qe1 = (qb < nq && qb != qe0) ? qb : -1;
-    const int my_edge = tg == 0 ? qe0 : (tg == 1 ? qe1 : -1);
-    auto masked = [&](int q, float fill) -> float4 {
-      float4 v = sl4[q];
-      const int e0 = 4 * q - phase;
-      if (e0 + 0 < 0 || e0 + 0 >= V) v.x = fill;
-      if (e0 + 1 < 0 || e0 + 1 >= V) v.y = fill;
-      if (e0 + 2 < 0 || e0 + 2 >= V) v.z = fill;
-      if (e0 + 3 < 0 || e0 + 3 >= V) v.w = fill;
-      return v;
-    };
-    auto min4 = [](float a, const float4& v) { return fminf(fminf(a, fminf(v.x, v.y)), fminf(v.z, v.w)); };
-    auto max4 = [](float a, const float4& v) { return fmaxf(fmaxf(a, fmaxf(v.x, v.y)), fmaxf(v.z, v.w)); };
-
-    float M = 0.0f, r = 0.0f;
-    double rd = 0.0;
-    bool bad;
-    float mn = -kNegInf;
-    if constexpr (ALG == osmx_host::kOnline) {
-      // Alg. 3 lines 1-6: per thread, batch max first then one rescale.
-      L2Acc acc;
-      constexpr int U = 4;
-      int q = qa + tg;
-      for (; q + (U - 1) * GT < qb; q += U * GT) {
-        float4 v[U];
-        float bm = kNegInf;
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          v[u] = sl4[q + u * GT];
-          mn = min4(mn, v[u]);
-          bm = max4(bm, v[u]);
+    long long j = g, k = 0;  // j: row sequence index in the cluster; k: this group's row count
+    for (long long row = cl + (long long)g * ncl; row < rows; row += (long long)NG * ncl, j += NG, ++k) {
+      const int s = (int)(j % D);
+      const int par = (int)(k & 1);
+      mbar_wait(&full[s], (uint32_t)((j / D) & 1));
+      const float* xs = x + row * ldx + s0;
+      float* ys = y + row * ldy + s0;
+      const int phase = (int)((reinterpret_cast<uintptr_t>(xs) >> 2) & 3);
+      const int nq = (phase + n + 3) >> 2;
+      const float4* sl4 = reinterpret_cast<const float4*>(slots + (size_t)s * slotf);
+      // Interior float4s [qa, qb) lie entirely inside the slice; the <= 2 edge
+      // float4s (qe0 = 0 when phase > 0, qe1 = qb when the slice ends
+      // mid-float4) are masked, one thread each.
+      const int qa = phase ? 1 : 0;
+      const int qb = (phase + n) >> 2 > qa ? (phase + n) >> 2 : qa;
+      const int qe0 = (phase && n > 0) ? 0 : -1;
+      const int qe1 = (qb < nq && qb != qe0) ? qb : -1;
+      const int my_edge = tg == 0 ? qe0 : (tg == 1 ? qe1 : -1);
+      auto masked = [&](int q, float fill) -> float4 {
+        float4 v = sl4[q];
+        const int e0 = 4 * q - phase;
+        if (e0 + 0 < 0 || e0 + 0 >= n) v.x = fill;
+        if (e0 + 1 < 0 || e0 + 1 >= n) v.y = fill;
+        if (e0 + 2 < 0 || e0 + 2 >= n) v.z = fill;
+        if (e0 + 3 < 0 || e0 + 3 >= n) v.w = fill;
+        return v;
+      };
+      auto min4 = [](float a, const float4& v) { return fminf(fminf(a, fminf(v.x, v.y)), fminf(v.z, v.w)); };
+      auto max4 = [](float a, const float4& v) { return fmaxf(fmaxf(a, fmaxf(v.x, v.y)), fmaxf(v.z, v.w)); };
+      // Cluster exchange, round r: send this group's record to group g of every
+      // CTA, wait for the C records of this row; returns them (rank order).
+      auto exchange = [&](int r, const SRecX& mine) -> const SRecX* {
+        const int b = (g * 2 + r) * 2 + par;
+        SRecX* buf = recs + (size_t)b * C;
+        if (tg == 0) {
+          mbar_arrive_expect_tx(&recbar[b], 16u * C);
+          for (unsigned q = 0; q < C; ++q) st_async_rec(&buf[c], &recbar[b], q, mine);
         }
-        acc.raise(bm);
-        acc.add_batch<U>(v);
-      }
-      for (; q < qb; q += GT) {
-        float4 v[1] = {sl4[q]};
-        mn = min4(mn, v[0]);
-        acc.raise(max4(kNegInf, v[0]));
-        acc.add_batch<1>(v);
-      }
-      if (my_edge >= 0) {
-        float4 v[1] = {masked(my_edge, kNegInf)};
-        mn = min4(mn, masked(my_edge, -kNegInf));
-        const float bm = max4(kNegInf, v[0]);
-        acc.raise(bm);
-        if (bm != kNegInf) acc.add_batch<1>(v);
-      }
-      const MD tot = SGrp<GW>::md(acc.finish(), scr, bar_id, lw);
-      mn = SGrp<GW>::red(mn, SOpMin(), scr, bar_id, lw);
-      M = tot.m;
-      r = __frcp_rn(tot.d);
-      bad = !(tot.d == tot.d) || !isfinite(M) || mn == kNegInf;
-    } else if constexpr (ALG == osmx_host::kSafe) {
-      // kernels.hpp:54 max, :56 sum against it
-      float m = kNegInf, chk = 0.0f;
-      for (int q = qa + tg; q < qb; q += GT) {
-        const float4 v = sl4[q];
-        mn = min4(mn, v);
-        m = max4(m, v);
-        chk = fmaf(v.x, 0.0f, fmaf(v.y, 0.0f, fmaf(v.z, 0.0f, fmaf(v.w, 0.0f, chk))));  // NaN iff inf/NaN
-      }
-      if (my_edge >= 0) {
-        const float4 v = masked(my_edge, kNegInf);
-        m = max4(m, v);
-        mn = min4(mn, masked(my_edge, -kNegInf));
-        const float4 z = masked(my_edge, 0.0f);  // out-of-row lanes must not poison chk
-        chk = fmaf(z.x, 0.0f, fmaf(z.y, 0.0f, fmaf(z.z, 0.0f, fmaf(z.w, 0.0f, chk))));
-      }
-      if (!(chk == chk)) mn = kNegInf;  // -inf survives the fminf group reduce (NaN would not)
-      M = SGrp<GW>::red(m, SOpMax(), scr, bar_id, lw);
-      mn = SGrp<GW>::red(mn, SOpMin(), scr, bar_id, lw);
-      L2Acc sacc;
-      sacc.raise(M);
-      for (int q = qa + tg; q < qb; q += GT) {
-        float4 v[1] = {sl4[q]};
-        sacc.add_batch<1>(v);
-      }
-      if (my_edge >= 0) {
-        float4 v[1] = {masked(my_edge, kNegInf)};
-        sacc.add_batch<1>(v);
-      }
-      float d = (M == kNegInf) ? 0.0f : sacc.finish().d;
-      d = SGrp<GW>::red(d, SOpSum(), scr, bar_id, lw);
-      r = __frcp_rn(d);
-      bad = !(d == d) || !isfinite(M) || !(mn == mn) || mn == kNegInf;
-    } else {
-      // naive: d = sum double(expf(x)) (kernels.hpp:43-44), no max shift
-      double d = 0.0;
-      float mx = kNegInf;
-      for (int q = qa + tg; q < qb; q += GT) {
-        const float4 v = sl4[q];
-        mn = min4(mn, v);
-        mx = max4(mx, v);
-        d += ((double)expf(v.x) + (double)expf(v.y)) + ((double)expf(v.z) + (double)expf(v.w));
-      }
-      if (my_edge >= 0) {
-        const float4 v = masked(my_edge, kNegInf);  // expf(-inf) = 0
-        mn = min4(mn, masked(my_edge, -kNegInf));
-        mx = max4(mx, v);
-        d += ((double)expf(v.x) + (double)expf(v.y)) + ((double)expf(v.z) + (double)expf(v.w));
-      }
-      d = SGrp<GW>::red(d, SOpSumD(), scrd, bar_id, lw);
-      mx = SGrp<GW>::red(mx, SOpMax(), scr, bar_id, lw);
-      mn = SGrp<GW>::red(mn, SOpMin(), scr, bar_id, lw);
-      rd = 1.0 / d;
-      bad = !(d == d) || !isfinite(mx) || mn == kNegInf;
-    }
-    if (bad && tg == 0) flag_bad_row(ws, row);
+        mbar_wait(&recbar[b], (uint32_t)((k >> 1) & 1));
+        return buf;
+      };
 
-    // Final pass: y = e^(x - m) / d (kernels.hpp:57 / :68; naive :45).
-    auto f = [&](float v) -> float {
-      if constexpr (ALG == osmx_host::kNaive)
-        return (float)((double)expf(v) * rd);
-      else
-        return expf(v - M) * r;
-    };
-    const bool same_phase = ((reinterpret_cast<uintptr_t>(yr) >> 2) & 3) == (uintptr_t)phase;
-    float* yb = yr - phase;  // yb[4q + c] <-> slot float4 q component c
-    if (same_phase) {
-      constexpr int U2 = 4;
-      int q = qa + tg;
-      for (; q + (U2 - 1) * GT < qb; q += U2 * GT) {
-        float4 v[U2];
+      float M = 0.0f, rr = 0.0f;
+      double rd = 0.0;
+      bool bad;
+      float mn = -kNegInf;
+      if constexpr (ALG == osmx_host::kOnline) {
+        // Alg. 3 lines 1-6: per thread, batch max first then one rescale.
+        L2Acc acc;
+        constexpr int U = 4;
+        int q = qa + tg;
+        for (; q + (U - 1) * GT < qb; q += U * GT) {
+          float4 v[U];
+          float bm = kNegInf;
 #pragma unroll
-        for (int u = 0; u < U2; ++u) v[u] = sl4[q + u * GT];
+          for (int u = 0; u < U; ++u) {
+            v[u] = sl4[q + u * GT];
+            mn = min4(mn, v[u]);
+            bm = max4(bm, v[u]);
+          }
+          acc.raise(bm);
+          acc.add_batch<U>(v);
+        }
+        for (; q < qb; q += GT) {
+          float4 v[1] = {sl4[q]};
+          mn = min4(mn, v[0]);
+          acc.raise(max4(kNegInf, v[0]));
+          acc.add_batch<1>(v);
+        }
+        if (my_edge >= 0) {
+          float4 v[1] = {masked(my_edge, kNegInf)};
+          mn = min4(mn, masked(my_edge, -kNegInf));
+          const float bm = max4(kNegInf, v[0]);
+          acc.raise(bm);
+          if (bm != kNegInf) acc.add_batch<1>(v);
+        }
+        MD tot = SGrp<GW>::md(acc.finish(), scr, bar_id, lw);
+        mn = SGrp<GW>::red(mn, SOpMin(), scr, bar_id, lw);
+        if (C > 1) {
+          const SRecX* rec = exchange(0, SRecX{tot.m, mn, (double)tot.d});
+          tot = md_identity();
+          mn = -kNegInf;
+          for (unsigned q = 0; q < C; ++q) {
+            tot = md_merge(tot, MD{rec[q].m, (float)rec[q].d});
+            mn = fminf(mn, rec[q].mn);
+          }
+        }
+        M = tot.m;
+        rr = __frcp_rn(tot.d);
+        bad = !(tot.d == tot.d) || !isfinite(M) || mn == kNegInf;
+      } else if constexpr (ALG == osmx_host::kSafe) {
+        // kernels.hpp:54 max, :56 sum against it
+        float m = kNegInf, chk = 0.0f;
+        for (int q = qa + tg; q < qb; q += GT) {
+          const float4 v = sl4[q];
+          mn = min4(mn, v);
+          m = max4(m, v);
+          chk = fmaf(v.x, 0.0f, fmaf(v.y, 0.0f, fmaf(v.z, 0.0f, fmaf(v.w, 0.0f, chk))));  // NaN iff inf/NaN
+        }
+        if (my_edge >= 0) {
+          m = max4(m, masked(my_edge, kNegInf));
+          mn = min4(mn, masked(my_edge, -kNegInf));
+          const float4 z = masked(my_edge, 0.0f);  // out-of-slice lanes must not poison chk
+          chk = fmaf(z.x, 0.0f, fmaf(z.y, 0.0f, fmaf(z.z, 0.0f, fmaf(z.w, 0.0f, chk))));
+        }
+        if (!(chk == chk)) mn = kNegInf;  // -inf survives the fminf group reduce (NaN would not)
+        M = SGrp<GW>::red(m, SOpMax(), scr, bar_id, lw);
+        mn = SGrp<GW>::red(mn, SOpMin(), scr, bar_id, lw);
+        if (C > 1) {
+          const SRecX* rec = exchange(0, SRecX{M, mn, 0.0});
+          M = kNegInf;
+          mn = -kNegInf;
+          for (unsigned q = 0; q < C; ++q) {
+            M = fmaxf(M, rec[q].m);
+            mn = fminf(mn, rec[q].mn);
+          }
+        }
+        L2Acc sacc;
+        sacc.raise(M);
+        for (int q = qa + tg; q < qb; q += GT) {
+          float4 v[1] = {sl4[q]};
+          sacc.add_batch<1>(v);
+        }
+        if (my_edge >= 0) {
+          float4 v[1] = {masked(my_edge, kNegInf)};
+          sacc.add_batch<1>(v);
+        }
+        float d = (M == kNegInf) ? 0.0f : sacc.finish().d;
+        d = SGrp<GW>::red(d, SOpSum(), scr, bar_id, lw);
+        if (C > 1) {
+          const SRecX* rec = exchange(1, SRecX{M, mn, (double)d});
+          d = 0.0f;
+          for (unsigned q = 0; q < C; ++q) d += (float)rec[q].d;
+        }
+        rr = __frcp_rn(d);
+        bad = !(d == d) || !isfinite(M) || !(mn == mn) || mn == kNegInf;
+      } else {
+        // naive: d = sum double(expf(x)) (kernels.hpp:43-44), no max shift
+        double d = 0.0;
+        float mx = kNegInf;
+        for (int q = qa + tg; q < qb; q += GT) {
+          const float4 v = sl4[q];
+          mn = min4(mn, v);
+          mx = max4(mx, v);
+          d += ((double)expf(v.x) + (double)expf(v.y)) + ((double)expf(v.z) + (double)expf(v.w));
+        }
+        if (my_edge >= 0) {
+          const float4 v = masked(my_edge, kNegInf);  // expf(-inf) = 0
+          mn = min4(mn, masked(my_edge, -kNegInf));
+          mx = max4(mx, v);
+          d += ((double)expf(v.x) + (double)expf(v.y)) + ((double)expf(v.z) + (double)expf(v.w));
+        }
+        d = SGrp<GW>::red(d, SOpSumD(), scrd, bar_id, lw);
+        mx = SGrp<GW>::red(mx, SOpMax(), scr, bar_id, lw);
+        mn = SGrp<GW>::red(mn, SOpMin(), scr, bar_id, lw);
+        if (C > 1) {
+          const SRecX* rec = exchange(0, SRecX{mx, mn, d});
+          d = 0.0;
+          mx = kNegInf;
+          mn = -kNegInf;
+          for (unsigned q = 0; q < C; ++q) {
+            d += rec[q].d;
+            mx = fmaxf(mx, rec[q].m);
+            mn = fminf(mn, rec[q].mn);
+          }
+        }
+        rd = 1.0 / d;
+        bad = !(d == d) || !isfinite(mx) || mn == kNegInf;
+      }
+      if (bad && tg == 0 && c == 0) flag_bad_row(ws, row);
+
+      // Final pass: y = e^(x - m) / d (kernels.hpp:57 / :68; naive :45).
+      auto f = [&](float v) -> float {
+        if constexpr (ALG == osmx_host::kNaive)
+          return (float)((double)expf(v) * rd);
+        else
+          return expf(v - M) * rr;
+      };
+      const bool same_phase = ((reinterpret_cast<uintptr_t>(ys) >> 2) & 3) == (uintptr_t)phase;
+      float* yb = ys - phase;  // yb[4q + c] <-> slot float4 q component c
+      if (same_phase) {
+        constexpr int U2 = 4;
+        int q = qa + tg;
+        for (; q + (U2 - 1) * GT < qb; q += U2 * GT) {
+          float4 v[U2];
 #pragma unroll
-        for (int u = 0; u < U2; ++u)
-          st_f4(yb + 4 * (q + u * GT), make_float4(f(v[u].x), f(v[u].y), f(v[u].z), f(v[u].w)));
+          for (int u = 0; u < U2; ++u) v[u] = sl4[q + u * GT];
+#pragma unroll
+          for (int u = 0; u < U2; ++u)
+            st_f4(yb + 4 * (q + u * GT), make_float4(f(v[u].x), f(v[u].y), f(v[u].z), f(v[u].w)));
+        }
+        for (; q < qb; q += GT) {
+          const float4 v = sl4[q];
+          st_f4(yb + 4 * q, make_float4(f(v.x), f(v.y), f(v.z), f(v.w)));
+        }
+      } else {
+        for (int q = qa + tg; q < qb; q += GT) {
+          const float4 v = sl4[q];
+          float* d = yb + 4 * q;
+          st_f1(d + 0, f(v.x));
+          st_f1(d + 1, f(v.y));
+          st_f1(d + 2, f(v.z));
+          st_f1(d + 3, f(v.w));
+        }
       }
-      for (; q < qb; q += GT) {
-        const float4 v = sl4[q];
-        st_f4(yb + 4 * q, make_float4(f(v.x), f(v.y), f(v.z), f(v.w)));
+      if (my_edge >= 0) {
+        const float4 v = sl4[my_edge];
+        const int e0 = 4 * my_edge - phase;
+        if (e0 + 0 >= 0 && e0 + 0 < n) st_f1(ys + e0 + 0, f(v.x));
+        if (e0 + 1 >= 0 && e0 + 1 < n) st_f1(ys + e0 + 1, f(v.y));
+        if (e0 + 2 >= 0 && e0 + 2 < n) st_f1(ys + e0 + 2, f(v.z));
+        if (e0 + 3 >= 0 && e0 + 3 < n) st_f1(ys + e0 + 3, f(v.w));
       }
-    } else {
-      for (int q = qa + tg; q < qb; q += GT) {
-        const float4 v = sl4[q];
-        float* d = yb + 4 * q;
-        st_f1(d + 0, f(v.x));
-        st_f1(d + 1, f(v.y));
-        st_f1(d + 2, f(v.z));
-        st_f1(d + 3, f(v.w));
-      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
     }
-    if (my_edge >= 0) {
-      const float4 v = sl4[my_edge];
-      const int e0 = 4 * my_edge - phase;
-      if (e0 + 0 >= 0 && e0 + 0 < V) st_f1(yr + e0 + 0, f(v.x));
-      if (e0 + 1 >= 0 && e0 + 1 < V) st_f1(yr + e0 + 1, f(v.y));
-      if (e0 + 2 >= 0 && e0 + 2 < V) st_f1(yr + e0 + 2, f(v.z));
-      if (e0 + 3 >= 0 && e0 + 3 < V) st_f1(yr + e0 + 3, f(v.w));
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
   }
+  __syncwarp();          // reconverge warp 0 (lane 0 ran the producer loop)
+  if (C > 1) cl_sync();  // no CTA exits while a peer may still st.async into it
 }
 
-// Largest dynamic shared memory the staged kernels use per CTA.
 constexpr int kStagedSmemMax = 227 * 1024;
+constexpr long long kStagedMaxV = 16384;   // one CTA per row up to here
+constexpr long long kClusterSlice = 12288;  // target slice per CTA above
+constexpr long long kClusterMaxV = 10 * kClusterSlice;  // clusters of > 10 CTAs pack badly into GPCs (measured)
 
+// Launch one (GW, NG, C) layout.  NG is clamped so that D >= NG + 1.
 template <int GW, int ALG>
 cudaError_t run_staged_cfg(const float* x, long long ldx, float* y, long long ldy, long long rows, long long V,
-                           void* ws, cudaStream_t st, int ng, int ring_kb) {
+                           void* ws, cudaStream_t st, int ng, int ring_kb, int C) {
   const auto& tn = osmx_host::tuning();
   if (tn.staged_kb > 0) ring_kb = tn.staged_kb;
   if (tn.staged_ng > 0) ng = tn.staged_ng;
-  const size_t slot = (size_t)staged_slot_floats(V) * 4;
-  const size_t ring = std::min<size_t>((size_t)ring_kb * 1024, kStagedSmemMax) - staged_slots_off();
-  int D = (int)std::min<size_t>(ring / slot, kStagedMaxD);
-  ng = std::min(ng, std::min(D, 31 / GW));
-  if (ng < 1) return cudaErrorInvalidValue;
-  const int ctas_per_sm = std::max(1, (228 * 1024) / (ring_kb * 1024 + 1024));
-  const size_t smem = staged_slots_off() + (size_t)D * slot;
+  const int Sv = (int)(((V + C - 1) / C + 3) / 4 * 4);
+  const size_t slot = (size_t)staged_slot_floats(Sv) * 4;
+  ng = std::min(ng, 31 / GW);
+  int D = 0;
+  for (int it = 0; it < 3; ++it) {  // ng and the header size depend on each other (C > 1)
+    const size_t avail = (size_t)std::min(ring_kb * 1024, kStagedSmemMax) - staged_slots_off(ng, C);
+    D = (int)std::min<size_t>(avail / slot, kStagedMaxD);
+    if (D >= 2) ng = std::min(ng, D - 1);
+  }
+  if (D < 1 || ng < 1 || D < ng) return cudaErrorInvalidValue;
+  const size_t smem = staged_slots_off(ng, C) + (size_t)D * slot;
+  auto kern = k_softmax_staged<GW, ALG>;
   static bool attr_set = false;  // per instantiation; the attribute is per function
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_softmax_staged<GW, ALG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         kStagedSmemMax);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kStagedSmemMax);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  const long long grid = std::min<long long>(rows, (long long)osmx_host::num_sms() * ctas_per_sm);
-  k_softmax_staged<GW, ALG><<<(unsigned)grid, 32 * (1 + GW * ng), smem, st>>>(x, ldx, y, ldy, rows, (int)V, D, ws);
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(32 * (1 + GW * ng));
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  long long ncl;
+  if (C == 1) {
+    const int ctas_per_sm = std::max(1, (228 * 1024) / (int)(smem + 1024));
+    ncl = std::min<long long>(rows, (long long)osmx_host::num_sms() * ctas_per_sm);
+  } else {
+    cfg.gridDim = dim3((unsigned)(C * osmx_host::num_sms()));
+    int max_clusters = 0;
+    cudaError_t e = cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg);
+    if (e != cudaSuccess) return e;
+    if (max_clusters < 1) return cudaErrorInvalidConfiguration;
+    ncl = std::min<long long>(rows, max_clusters);
+  }
+  cfg.gridDim = dim3((unsigned)(ncl * C));
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, x, ldx, y, ldy, rows, (int)V, Sv, D, ws);
   osmx_host::count_launch();
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
-// Largest V served by the staged family (3 slots of a 200 KB ring).
-constexpr long long kStagedMaxV = 16384;
+// Cluster size for a row of V elements (1 up to kStagedMaxV).
+inline int staged_cluster_size(long long V) {
+  const int forced = osmx_host::tuning().cluster_size;
+  if (forced > 0) return forced;
+  if (V <= kStagedMaxV) return 1;
+  const long long c = (V + kClusterSlice - 1) / kClusterSlice;
+  return (int)std::min<long long>(c, 16);
+}
 
 template <int ALG>
 cudaError_t run_staged(const float* x, long long ldx, float* y, long long ldy, long long rows, long long V,
                        void* ws, cudaStream_t st) {
-  // Group width (warps per row) and group count per V, from
+  // Group width (warps per slice) and group count per slice length, from
   // tools/shape_sweep.py on B200 (4000 and 32768 rows, gw x ng grid,
-  // profiles/r01s2_staged_sweep.md): 2-warp groups x 6 up to V = 4096,
-  // 4-warp groups x 6 up to 8192, x 3 above; at least one slot stays in
-  // flight (ng <= D - 1), which matters once only 3-5 rows fit the ring.
+  // profiles/r01s2_staged_sweep.md): 2-warp groups x 6 up to 4096, 4-warp
+  // groups x 6 up to 8192, x 3 above; at least one slot stays in flight.
+  const int C = staged_cluster_size(V);
+  const long long Sv = (V + C - 1) / C;
   int gw = osmx_host::tuning().staged_gw;
   const int kb = 220;
-  if (gw == 0) gw = V <= 1024 ? 1 : V <= 4096 ? 2 : 4;
-  int ng = gw == 1 ? 16 : V <= 8192 ? 6 : 3;
-  {
-    const size_t slot = (size_t)staged_slot_floats(V) * 4;
-    const int D = (int)std::min<size_t>((size_t)(kb * 1024 - staged_slots_off()) / slot, kStagedMaxD);
-    if (D >= 2) ng = std::min(ng, D - 1);
-  }
+  if (gw == 0) gw = Sv <= 1024 ? 1 : Sv <= 4096 ? 2 : 4;
+  const int ng = gw == 1 ? 16 : Sv <= 8192 ? 6 : 3;
   switch (gw) {
-    case 1: return run_staged_cfg<1, ALG>(x, ldx, y, ldy, rows, V, ws, st, ng, kb);
-    case 2: return run_staged_cfg<2, ALG>(x, ldx, y, ldy, rows, V, ws, st, ng, kb);
-    case 4: return run_staged_cfg<4, ALG>(x, ldx, y, ldy, rows, V, ws, st, ng, kb);
-    case 8: return run_staged_cfg<8, ALG>(x, ldx, y, ldy, rows, V, ws, st, ng, kb);
-    default: return run_staged_cfg<16, ALG>(x, ldx, y, ldy, rows, V, ws, st, ng, kb);
+    case 1: return run_staged_cfg<1, ALG>(x, ldx, y, ldy, rows, V, ws, st, ng, kb, C);
+    case 2: return run_staged_cfg<2, ALG>(x, ldx, y, ldy, rows, V, ws, st, ng, kb, C);
+    case 4: return run_staged_cfg<4, ALG>(x, ldx, y, ldy, rows, V, ws, st, ng, kb, C);
+    case 8: return run_staged_cfg<8, ALG>(x, ldx, y, ldy, rows, V, ws, st, ng, kb, C);
+    default: return run_staged_cfg<16, ALG>(x, ldx, y, ldy, rows, V, ws, st, ng, kb, C);
   }
 }
 

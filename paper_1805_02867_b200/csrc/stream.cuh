@@ -50,13 +50,16 @@ __device__ __forceinline__ long long body_index(const Seg& s, long long q, int c
 // Visit every element of the segment once:
 //   f1(x, j)                    scalar element j
 //   fb(v[U], q0, cnt)           cnt (<= U) float4s at body indices q0 + u*G
-// LAST selects the evict-first load flavour (final read of the data).
+// LAST = 1 selects the evict-first load flavour (final read of the data),
+// LAST = 2 the evict-last one (data re-read soon by the same CTA).
 // pf > 0: thread 0 of the group keeps the group's body pf batches ahead in
 // L2 with bulk prefetches, so the demand loads see L2 rather than DRAM
 // latency without spending registers on more loads in flight.
-template <int G, int U, bool LAST, class F1, class FB>
+template <int G, int U, int LAST, class F1, class FB>
 __device__ __forceinline__ void stream_seg(const Seg& s, int t, F1&& f1, FB&& fb, int pf = 0) {
-  if (t < s.head) f1(LAST ? ld_f1_last(s.p + t) : ld_f1(s.p + t), (long long)t);
+  auto L4 = [](const float* p) { return LAST == 1 ? ld_f4_last(p) : LAST == 2 ? ld_f4_keep(p) : ld_f4(p); };
+  auto L1 = [](const float* p) { return LAST == 1 ? ld_f1_last(p) : LAST == 2 ? ld_f1_keep(p) : ld_f1(p); };
+  if (t < s.head) f1(L1(s.p + t), (long long)t);
   const float* b = s.p + s.head;
   constexpr long long kB = (long long)U * G;  // float4s per batch of the group
   if (pf > 0 && t == 0 && s.nvec > 0) {
@@ -71,7 +74,7 @@ __device__ __forceinline__ void stream_seg(const Seg& s, int t, F1&& f1, FB&& fb
     }
     float4 v[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) v[u] = LAST ? ld_f4_last(b + 4 * (q + (long long)u * G)) : ld_f4(b + 4 * (q + (long long)u * G));
+    for (int u = 0; u < U; ++u) v[u] = L4(b + 4 * (q + (long long)u * G));
     fb(v, q, U);
   }
   if (q < s.nvec) {
@@ -81,7 +84,7 @@ __device__ __forceinline__ void stream_seg(const Seg& s, int t, F1&& f1, FB&& fb
     for (int u = 0; u < U; ++u) {
       const long long qq = q + (long long)u * G;
       if (qq < s.nvec) {
-        v[u] = LAST ? ld_f4_last(b + 4 * qq) : ld_f4(b + 4 * qq);
+        v[u] = L4(b + 4 * qq);
         cnt = u + 1;
       } else {
         v[u] = make_float4(kNegInf, kNegInf, kNegInf, kNegInf);
@@ -91,7 +94,79 @@ __device__ __forceinline__ void stream_seg(const Seg& s, int t, F1&& f1, FB&& fb
   }
   if (t < s.tail) {
     const long long j = s.head + 4 * s.nvec + t;
-    f1(LAST ? ld_f1_last(s.p + j) : ld_f1(s.p + j), j);
+    f1(L1(s.p + j), j);
+  }
+}
+
+// Same visit order as stream_seg for one warp (G = 32), but the body is
+// software-pipelined through shared memory: each lane keeps NST - 1 batches
+// of U float4s in flight with 16-byte cp.async (LDGSTS, L2 only) into its own
+// slots of `wbuf` ([NST][U][32] float4s, private to the warp), so the loads
+// of the next batches overlap the compute of this one without extra
+// registers.  Each lane reads back only what it wrote: no barrier needed.
+__device__ __forceinline__ void cp_async16(float4* dst, const float* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int U, int NST, class F1, class FB>
+__device__ __forceinline__ void stream_seg_pipe(const Seg& s, int t, F1&& f1, FB&& fb, float4* wbuf) {
+  if (t < s.head) f1(ld_f1(s.p + t), (long long)t);
+  constexpr int kB = U * 32;                      // float4s per batch of the warp
+  const int nvec = (int)s.nvec;                   // rows < 2^33 elements (host-checked)
+  const int nfull = nvec / kB, nb = (nvec + kB - 1) / kB;
+  const float* ip = s.p + s.head + 4 * t;         // this lane's float4 of the next batch to issue
+  float4* const wl = wbuf + t;                    // this lane's slot of stage 0
+  int issued = 0, is = 0;
+  auto issue = [&]() {
+    if (issued < nfull) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) cp_async16(wl + is * kB + u * 32, ip + u * 128);
+    } else if (issued < nb) {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (issued * kB + u * 32 + t < nvec) cp_async16(wl + is * kB + u * 32, ip + u * 128);
+    }
+    cp_async_commit();
+    ip += 4 * kB;
+    ++issued;
+    is = is + 1 == NST ? 0 : is + 1;
+  };
+#pragma unroll
+  for (int i = 0; i < NST - 1; ++i) issue();
+  int cs = 0;
+  for (int bi = 0; bi < nb; ++bi) {
+    issue();
+    cp_async_wait<NST - 1>();
+    float4 v[U];
+    int cnt = U;
+    if (bi < nfull) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = wl[cs * kB + u * 32];
+    } else {
+      cnt = 0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (bi * kB + u * 32 + t < nvec) {
+          v[u] = wl[cs * kB + u * 32];
+          cnt = u + 1;
+        } else {
+          v[u] = make_float4(kNegInf, kNegInf, kNegInf, kNegInf);
+        }
+      }
+    }
+    fb(v, (long long)(bi * kB + t), cnt);
+    cs = cs + 1 == NST ? 0 : cs + 1;
+  }
+  if (t < s.tail) {
+    const long long j = s.head + 4 * s.nvec + t;
+    f1(ld_f1(s.p + j), j);
   }
 }
 

@@ -95,10 +95,25 @@ struct Pass {
       want = bkey > L.thr() && bkey >= T;
     }
     if (__any_sync(mask, want)) {
-      if (want) {
+      // Raise T before inserting: the k-th largest of the lanes' bests
+      // (this batch included) is a valid lower bound of the row's k-th best
+      // (k distinct elements >= it), so only elements >= it are offered --
+      // in the first batch that is ~k elements per warp instead of all.
+      if (__popc(mask) >= kk) {
+        int mine = f2o(best), kth = mine;
+        for (int r = 0; r < kk; ++r) {
+          kth = __reduce_max_sync(mask, mine);
+          const unsigned who = __ballot_sync(mask, mine == kth);
+          if ((int)(threadIdx.x & 31) == __ffs(who) - 1) mine = f2o(kNegInf);
+        }
+        T = fmaxf(T, o2f(kth));
+      }
+      if (bkey > L.thr() && bkey >= T) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           if (u >= cnt) break;  // padding of the last batch is never offered
+          // key is monotone: one test per float4 before the per-element ones
+          if (!(key(fmaxf(fmaxf(v[u].x, v[u].y), fmaxf(v[u].z, v[u].w))) >= T)) continue;
           const int j = j0 + u * jstride;
           const float k0 = key(v[u].x), k1 = key(v[u].y), k2 = key(v[u].z), k3 = key(v[u].w);
           if (k0 >= T) L.offer(k0, j);
@@ -107,19 +122,8 @@ struct Pass {
           if (k3 >= T) L.offer(k3, j + 3);
         }
       }
-      // Two valid lower bounds of the row's k-th best: the best lane k-th,
-      // and the k-th largest of the lanes' bests (k distinct elements >= it).
-      int t = __reduce_max_sync(mask, f2o(L.thr()));
-      if (__popc(mask) >= kk) {
-        int mine = f2o(best), kth = mine;
-        for (int r = 0; r < kk; ++r) {
-          kth = __reduce_max_sync(mask, mine);
-          const unsigned who = __ballot_sync(mask, mine == kth);
-          if ((int)(threadIdx.x & 31) == __ffs(who) - 1) mine = f2o(kNegInf);
-        }
-        t = max(t, kth);
-      }
-      T = fmaxf(T, o2f(t));
+      // the best lane k-th is a lower bound too
+      T = fmaxf(T, o2f(__reduce_max_sync(mask, f2o(L.thr()))));
       if (Tsh && (int)(threadIdx.x & 31) == __ffs(mask) - 1) atomicMax(Tsh, f2o(T));
     }
   }
@@ -235,12 +239,16 @@ __device__ __forceinline__ void cta_merge(TopList<KC>& L, int k, float* sv, int*
 // ---------------------------------------------------------- row kernel --
 // G threads per row (G == 32: warp per row, BLOCK/32 rows per CTA; G ==
 // BLOCK: CTA per row).  Rows are visited grid-stride.
-template <int G, int BLOCK, int KC, int MODE, int U, int MINB>
+// NST > 0 (warp per row only): the body streams through a per-warp
+// cp.async shared-memory pipeline of NST stages (stream_seg_pipe).
+template <int G, int BLOCK, int KC, int MODE, int U, int MINB, int NST = 0>
 __global__ void __launch_bounds__(BLOCK, MINB)
     k_topk_rows(const float* __restrict__ x, long long ldx, long long rows, long long V, int k,
                 float* __restrict__ vals, long long* __restrict__ idx, void* ws, int pf) {
   constexpr int NW = BLOCK / 32;
   constexpr int RPC = BLOCK / G;
+  static_assert(NST == 0 || G == 32, "the cp.async pipeline is per warp");
+  __shared__ __align__(16) float4 pipe_buf[NST > 0 ? NW * NST * U * 32 : 1];
   __shared__ float smf[2 * NW];
   __shared__ float sv[NW * KC];
   __shared__ int si[NW * KC];
@@ -283,7 +291,14 @@ __global__ void __launch_bounds__(BLOCK, MINB)
       P.R = __frcp_rn(d);
       bad = !(d == d) || !isfinite(M) || !(MN == MN) || MN == kNegInf;
     }
-    run_pass<G, U, KC, MODE>(P, s, t, k, pf);
+    if constexpr (NST > 0 && MODE != kModeSafe) {
+      stream_seg_pipe<U, NST>(
+          s, t, [&](float v, long long j) { P.scalar(v, (int)j, k); },
+          [&](float4 (&v)[U], long long q0, int cnt) { P.batch(s, v, q0, cnt, k); },
+          pipe_buf + (threadIdx.x >> 5) * (NST * U * 32));
+    } else {
+      run_pass<G, U, KC, MODE>(P, s, t, k, pf);
+    }
     if constexpr (MODE == kModeFused) {
       MD tot;
       float MN;
@@ -488,7 +503,17 @@ cudaError_t run_rows(const float* x, long long ldx, long long rows, long long V,
   // measured (tools/shape_sweep.py, 4000 rows): +8-9% at V = 16K-32K, +1% at
   // 64K, -2% at 128K (rows long enough to amortise the serial load->compute).
   if (u8 < 0) u8 = (g == 32 && V >= 8192 && V <= 65536 && rows <= 28LL * osmx_host::num_sms()) ? 1 : 0;
-  if (g == 32 && u8) {
+  const int pipe = V < (1LL << 33) ? osmx_host::tuning().topk_pipe : 0;  // 32-bit float4 counts
+  if (g == 32 && pipe > 0) {
+    // per-warp cp.async pipeline: 4-warp CTAs, U float4s x NST stages per lane
+    const long long grid = std::min<long long>((rows + 3) / 4, 1LL << 30);
+    if (pipe == 1)
+      k_topk_rows<32, 128, KC, MODE, 4, 8, 3><<<(unsigned)grid, 128, 0, st>>>(x, ldx, rows, V, k, vals, idx, ws, pf);
+    else if (pipe == 2)
+      k_topk_rows<32, 128, KC, MODE, 2, 8, 4><<<(unsigned)grid, 128, 0, st>>>(x, ldx, rows, V, k, vals, idx, ws, pf);
+    else
+      k_topk_rows<32, 128, KC, MODE, 4, 7, 2><<<(unsigned)grid, 128, 0, st>>>(x, ldx, rows, V, k, vals, idx, ws, pf);
+  } else if (g == 32 && u8) {
     // One wave of rows (<= 28 warps per SM): occupancy is set by the row
     // count, not by registers, so each lane keeps 8 float4s in flight
     // (4-warp CTAs, <= 72 registers: 7 CTAs = 28 warps per SM).

@@ -17,12 +17,14 @@ from tests._util import DISTS, dist, max_rel
 pytestmark = pytest.mark.gpu
 
 TOL = 1e-5
-SHAPES = {"auto": 0, "resident": 1, "stream": 2, "split": 3, "staged": 4}
+SHAPES = {"auto": 0, "resident": 1, "stream": 2, "split": 3, "staged": 4, "cluster": 5}
 # top-K launch variants: knob settings applied on top of the shape
 TOPK_VARIANTS = {
     "auto": [], "stream": [("shape", 2)], "split": [("shape", 3), ("split_chunk", 2048)], "tma": [("tma", 2)],
     "warp": [("topk_threads", 32), ("topk_u8", 0)], "warp_u8": [("topk_threads", 32), ("topk_u8", 1)],
     "warp_pf": [("topk_threads", 32), ("l2_prefetch", 2)], "cta_pf": [("topk_threads", 256), ("l2_prefetch", 1)],
+    "warp_pipe1": [("topk_threads", 32), ("topk_pipe", 1)], "warp_pipe2": [("topk_threads", 32), ("topk_pipe", 2)],
+    "warp_pipe3": [("topk_threads", 32), ("topk_pipe", 3)],
 }
 
 
@@ -33,7 +35,7 @@ def lib():
     _lib.load()
     yield _lib
     for key, val in (("shape", 0), ("split_chunk", 0), ("tma", 0), ("topk_threads", 0), ("topk_u8", -1),
-                     ("l2_prefetch", 0)):
+                     ("l2_prefetch", 0), ("cluster_size", 0), ("topk_pipe", 0)):
         _lib.config_set(key, val)
 
 
@@ -46,7 +48,7 @@ def _dev(x):
 SOFTMAX_V = [1, 2, 3, 5, 10, 17, 32, 33, 100, 255, 256, 1000, 1023, 1025, 2048, 4099, 8192, 16384, 16387, 70001]
 
 
-@pytest.mark.parametrize("shape", ["auto", "resident", "stream", "split", "staged"])
+@pytest.mark.parametrize("shape", ["auto", "resident", "stream", "split", "staged", "cluster"])
 @pytest.mark.parametrize("alg", ["naive", "safe", "online"])
 def test_softmax_parity(cuda, oracle_mod, lib, alg, shape):
     from paper_1805_02867_b200 import osmx
@@ -82,10 +84,11 @@ def test_softmax_strided_and_misaligned(cuda, oracle_mod, lib, alg):
     from paper_1805_02867_b200 import osmx
 
     rng = np.random.default_rng(7)
-    for shape in (0, 2, 3, 4):
+    for shape in (0, 2, 3, 4, 5):
         lib.config_set("shape", shape)
         lib.config_set("split_chunk", 4096 if shape == 3 else 0)
-        for V in (5, 999, 4097, 20001):
+        lib.config_set("cluster_size", 4 if shape == 5 else 0)
+        for V in (5, 999, 4097, 20001, 70003):
             big = rng.standard_normal((6, V + 7)).astype(np.float32)
             xt = torch.from_numpy(big).cuda()[:, 1 : V + 1]  # ld = V+7, base offset 4 bytes
             y = osmx.softmax(xt, alg=alg).cpu().numpy()
@@ -274,9 +277,10 @@ def test_nonfinite_rows_flagged(cuda, lib):
     from paper_1805_02867_b200 import osmx
 
     rng = np.random.default_rng(5)
-    for shape in (0, 1, 2, 3, 4):
+    for shape in (0, 1, 2, 3, 4, 5):
         lib.config_set("shape", shape)
         lib.config_set("split_chunk", 2048 if shape == 3 else 0)
+        lib.config_set("cluster_size", 2 if shape == 5 else 0)
         for bad in (np.nan, np.inf, -np.inf):
             for V in (7, 3000, 40000):
                 if shape in (1, 4) and V > 16384:
@@ -329,7 +333,7 @@ def test_softmax_staged_ring_wrap(cuda, oracle_mod, lib, alg):
         assert max_rel(y, ref) <= TOL, (alg, V)
 
 
-@pytest.mark.parametrize("variant", ["auto", "warp", "warp_u8", "warp_pf"])
+@pytest.mark.parametrize("variant", ["auto", "warp", "warp_u8", "warp_pf", "warp_pipe1", "warp_pipe3"])
 def test_online_fused_topk_many_rows(cuda, oracle_mod, lib, variant):
     """Row counts around one wave of warps (the u8 heuristic's range)."""
     from paper_1805_02867_b200 import osmx
@@ -343,3 +347,23 @@ def test_online_fused_topk_many_rows(cuda, oracle_mod, lib, variant):
         rv, rz = _topk_ref(oracle_mod, "online_softmax_topk", x, 5)
         assert np.array_equal(idx.cpu().numpy(), rz), (variant, rows, V)
         assert max_rel(vals.cpu().numpy(), rv) <= TOL
+
+
+@pytest.mark.parametrize("alg", ["online", "safe", "naive"])
+def test_softmax_cluster_slices(cuda, oracle_mod, lib, alg):
+    """Rows split over 2..16 CTAs of a cluster (distributed shared memory
+    merge), including empty slices (V < C * 4) and enough rows that every
+    ring slot and record parity is reused."""
+    from paper_1805_02867_b200 import osmx
+
+    lib.config_set("shape", SHAPES["cluster"])
+    rng = np.random.default_rng(13)
+    for V, C, rows in ((70001, 0, 300), (16387, 2, 400), (100003, 4, 200), (300001, 16, 48), (5, 4, 33),
+                       (40000, 8, 64)):
+        lib.config_set("cluster_size", C)
+        for d in ("normal", "spikes", "quantized2"):
+            x = dist(d, rng, rows, V)
+            y = osmx.softmax(_dev(x), alg=alg).cpu().numpy()
+            ref, st = oracle_mod.batch(f"{alg}_softmax", x)
+            assert (st == 0).all()
+            assert max_rel(y, ref) <= TOL, (alg, V, C, d)
