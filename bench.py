@@ -243,6 +243,7 @@ def main() -> None:
     ap.add_argument("--e2e", default="auto", choices=["auto", "on", "off"])
     ap.add_argument("--cpu", default="auto", choices=["auto", "on", "off"])
     ap.add_argument("--sweep-reps", type=int, default=10)
+    ap.add_argument("--sweep-only", action="store_true", help="print only the configs[1]/[2]/[4] sweeps (N=1)")
     args = ap.parse_args()
 
     if args.impl == "reference":
@@ -257,6 +258,17 @@ def main() -> None:
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    if args.sweep_only:
+        from paper_1805_02867_b200 import _lib
+
+        lib = _lib.load()
+        ss = ClockSampler(local)
+        ss.start()
+        sweep = run_sweeps(lib, _lib, dev, torch.cuda.current_stream(dev).cuda_stream, args.sweep_reps,
+                           measured_peaks()["hbm_gbs"])
+        sweep["clocks"] = ss.stop()
+        print(json.dumps({"metric": METRIC, "sweep": sweep}), flush=True)
+        return
     dist = None
     if world > 1:
         import torch.distributed as dist
@@ -303,6 +315,15 @@ def main() -> None:
         gv = vals[sample].cpu().numpy()
         parity = {"rows_checked": len(sample), "indices_bit_exact": bool(np.array_equal(gi, rz)),
                   "max_rel_err": float(np.max(np.abs(gv.astype(np.float64) - rv) / rv))}
+
+    # ---- sweeps (N=1; configs[1], [2], [4]), before the headline timed region
+    sweep = None
+    if rank == 0 and world == 1 and (args.sweep == "on" or args.sweep == "auto"):
+        ss = ClockSampler(local)
+        ss.start()
+        sweep = run_sweeps(lib, _lib, dev, sp, args.sweep_reps, measured_peaks()["hbm_gbs"])
+        sweep["clocks"] = ss.stop()
+        torch.cuda.empty_cache()
 
     # ---- timed region
     if dist is not None:
@@ -388,11 +409,8 @@ def main() -> None:
     if rank == 0 and world == 1 and args.cpu != "off":
         result["cpu_baseline"] = cpu_baseline(x, V, k)
 
-    # ---- sweeps (N=1)
-    if rank == 0 and world == 1 and (args.sweep == "on" or args.sweep == "auto"):
-        del x
-        torch.cuda.empty_cache()
-        result["sweep"] = run_sweeps(lib, _lib, dev, sp, args.sweep_reps, peaks["hbm_gbs"])
+    if sweep is not None:
+        result["sweep"] = sweep
 
     if rank == 0:
         print(json.dumps(result), flush=True)
@@ -532,8 +550,13 @@ def run_sweeps(lib, _lib, dev, sp, reps, peak) -> dict:
         x = torch.empty((n, B, V), dtype=torch.float32, device=dev).normal_()
         y = torch.empty_like(x)
         row = {"V": V, "n_sets": n}
-        for name, alg in (("naive", _lib.NAIVE_SOFTMAX), ("safe", _lib.SAFE_SOFTMAX),
-                          ("online", _lib.ONLINE_SOFTMAX)):
+        # best kernel family per V (auto), and the paper's one-CTA-per-row
+        # streaming kernels (shape 2: every pass reads global memory; the
+        # safe baseline of the north star, 3 passes / 4 accesses)
+        for name, alg, shape in (("naive", _lib.NAIVE_SOFTMAX, 0), ("safe", _lib.SAFE_SOFTMAX, 0),
+                                 ("online", _lib.ONLINE_SOFTMAX, 0), ("safe_stream", _lib.SAFE_SOFTMAX, 2),
+                                 ("online_stream", _lib.ONLINE_SOFTMAX, 2)):
+            _lib.config_set("shape", shape)
             nb = lib.osmx_workspace_bytes(alg, B, V, 0)
             ws = torch.zeros(max(nb, 256), dtype=torch.uint8, device=dev)
 
@@ -541,11 +564,15 @@ def run_sweeps(lib, _lib, dev, sp, reps, peak) -> dict:
                 lib.osmx_softmax(alg, x[i].data_ptr(), V, y[i].data_ptr(), V, B, V, ws.data_ptr(), ws.numel(), st)
 
             ms, ms_min = time_rotating(launch, n, reps)
-            gbs = algo_bytes(name, B, V) / (ms * 1e-3) / 1e9
+            _lib.config_set("shape", 0)
+            gbs = algo_bytes(name.replace("_stream", ""), B, V) / (ms * 1e-3) / 1e9
             row[name] = {"ms": round(ms, 5), "GBps": round(gbs, 1), "frac": round(gbs / peak, 3),
                          "dram_floor_GBps": round(8 * B * V / (ms * 1e-3) / 1e9, 1),
                          "elements_per_s": round(B * V / (ms * 1e-3), 1)}
         row["online_over_safe"] = round(row["safe"]["ms"] / row["online"]["ms"], 3)
+        # the paper's comparison: both algorithms in the streaming kernel family
+        row["online_stream_over_safe_stream"] = round(row["safe_stream"]["ms"] / row["online_stream"]["ms"], 3)
+        row["online_over_safe_stream"] = round(row["safe_stream"]["ms"] / row["online"]["ms"], 3)
         out["softmax"].append(row)
         del x, y
         torch.cuda.empty_cache()
@@ -555,10 +582,12 @@ def run_sweeps(lib, _lib, dev, sp, reps, peak) -> dict:
         vals = torch.empty((B, k), dtype=torch.float32, device=dev)
         idx = torch.empty((B, k), dtype=torch.int64, device=dev)
         row = {"V": V, "n_sets": n}
-        for name, alg in (("online_fused", _lib.ONLINE_SOFTMAX_FUSED_TOPK),
-                          ("online_unfused", _lib.ONLINE_SOFTMAX_UNFUSED_TOPK),
-                          ("safe_unfused", _lib.SAFE_SOFTMAX_UNFUSED_TOPK),
-                          ("safe_fused", _lib.SAFE_SOFTMAX_FUSED_TOPK)):
+        for name, alg, shape in (("online_fused", _lib.ONLINE_SOFTMAX_FUSED_TOPK, 0),
+                                 ("online_unfused", _lib.ONLINE_SOFTMAX_UNFUSED_TOPK, 0),
+                                 ("safe_unfused", _lib.SAFE_SOFTMAX_UNFUSED_TOPK, 0),
+                                 ("safe_fused", _lib.SAFE_SOFTMAX_FUSED_TOPK, 0),
+                                 ("online_unfused_stream", _lib.ONLINE_SOFTMAX_UNFUSED_TOPK, 2)):
+            _lib.config_set("shape", shape)
             nb = lib.osmx_workspace_bytes(alg, B, V, k)
             ws = torch.zeros(max(nb, 256), dtype=torch.uint8, device=dev)
 
@@ -567,16 +596,55 @@ def run_sweeps(lib, _lib, dev, sp, reps, peak) -> dict:
                                       ws.data_ptr(), ws.numel(), st)
 
             ms, ms_min = time_rotating(launch, n, reps)
-            gbs = algo_bytes(name, B, V) / (ms * 1e-3) / 1e9
+            _lib.config_set("shape", 0)
+            gbs = algo_bytes(name.replace("_stream", ""), B, V) / (ms * 1e-3) / 1e9
             row[name] = {"ms": round(ms, 5), "GBps": round(gbs, 1), "frac": round(gbs / peak, 3),
                          "rows_per_s": round(B / (ms * 1e-3), 1)}
             del ws
         row["fused_over_online_unfused"] = round(row["online_unfused"]["ms"] / row["online_fused"]["ms"], 3)
         row["fused_over_safe_unfused"] = round(row["safe_unfused"]["ms"] / row["online_fused"]["ms"], 3)
+        # unfused pipeline whose softmax stage is the paper's 3-access streaming kernel
+        row["fused_over_online_unfused_stream"] = round(row["online_unfused_stream"]["ms"] / row["online_fused"]["ms"],
+                                                        3)
         out["topk"].append(row)
         del x
         torch.cuda.empty_cache()
+    out["c5"] = run_c5(lib, _lib, dev, reps, peak, l2)
     return out
+
+
+def run_c5(lib, _lib, dev, reps, peak, l2) -> dict:
+    """configs[4] on one GPU: a single row of V = 2^26 (256 MB), fused online
+    softmax + Top-5 and online softmax, split over CTAs with the (m, d) /
+    top-K record combine (the per-GPU leg of the NCCL V-split)."""
+    import torch
+
+    V, k = 1 << 26, K_TOP
+    n = n_rotating_sets(8 * V, l2)
+    x = torch.empty((n, V), dtype=torch.float32, device=dev).normal_()
+    y = torch.empty_like(x)
+    vals = torch.empty((1, k), dtype=torch.float32, device=dev)
+    idx = torch.empty((1, k), dtype=torch.int64, device=dev)
+    res = {"rows": 1, "V": V, "k": k, "n_sets": n}
+    for name, alg in (("online_fused", _lib.ONLINE_SOFTMAX_FUSED_TOPK), ("online", _lib.ONLINE_SOFTMAX)):
+        topk = name == "online_fused"
+        nb = lib.osmx_workspace_bytes(alg, 1, V, k if topk else 0)
+        ws = torch.zeros(max(nb, 256), dtype=torch.uint8, device=dev)
+
+        def launch(i, st, alg=alg, ws=ws, topk=topk):
+            if topk:
+                lib.osmx_softmax_topk(alg, x[i].data_ptr(), V, 1, V, k, vals.data_ptr(), idx.data_ptr(), ws.data_ptr(),
+                                      ws.numel(), st)
+            else:
+                lib.osmx_softmax(alg, x[i].data_ptr(), V, y[i].data_ptr(), V, 1, V, ws.data_ptr(), ws.numel(), st)
+
+        ms, _ = time_rotating(launch, n, reps)
+        gbs = algo_bytes(name, 1, V, k) / (ms * 1e-3) / 1e9
+        res[name] = {"ms": round(ms, 5), "GBps": round(gbs, 1), "frac": round(gbs / peak, 3),
+                     "elements_per_s": round(V / (ms * 1e-3), 1)}
+    del x, y
+    torch.cuda.empty_cache()
+    return res
 
 
 if __name__ == "__main__":

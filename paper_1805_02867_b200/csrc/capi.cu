@@ -61,6 +61,9 @@ static size_t split_region(int alg, long long rows, long long V, int k) {
     case kOnlineFusedTopk:
       if (topk_split(rows, V)) b = topk_split_ws(alg, rows, V, k);
       break;
+    case kSliceRecord:  // always the split path (piece records + combine)
+      b = topk_split_ws(kOnlineFusedTopk, rows, V, k);
+      break;
     case kSafeUnfusedTopk:
     case kOnlineUnfusedTopk:
     case kTopkOf: {
@@ -300,6 +303,9 @@ osmx_status osmx_config_set(const char* key, int64_t value) {
   } else if (!strcmp(key, "staged_kb")) {
     if (value != 0 && (value < 16 || value > 227)) return OSMX_ERR_INVALID_ARG;
     t.staged_kb = (int)value;
+  } else if (!strcmp(key, "split_cta")) {
+    if (value < 0 || value > 1) return OSMX_ERR_INVALID_ARG;
+    t.split_cta = (int)value;
   } else if (!strcmp(key, "topk_pipe")) {
     if (value < 0 || value > 3) return OSMX_ERR_INVALID_ARG;
     t.topk_pipe = (int)value;
@@ -333,6 +339,7 @@ int64_t osmx_config_get(const char* key) {
   if (!strcmp(key, "l2_prefetch")) return t.l2_prefetch;
   if (!strcmp(key, "topk_u8")) return t.topk_u8;
   if (!strcmp(key, "topk_pipe")) return t.topk_pipe;
+  if (!strcmp(key, "split_cta")) return t.split_cta;
   if (!strcmp(key, "stream_ctas")) return t.stream_ctas;
   if (!strcmp(key, "staged_gw")) return t.staged_gw;
   if (!strcmp(key, "cluster_size")) return t.cluster_size;

@@ -320,9 +320,14 @@ __global__ void __launch_bounds__(BLOCK)
       bad = !(d == d) || !isfinite(mx) || mn == kNegInf;
     }
     if (bad && t == 0) flag_bad_row(ws, row);
-    // Final pass: y = e^(x - m) / d (kernels.hpp:57 / :68; naive :45).
+    // Final pass: y = e^(x - m) / d (kernels.hpp:57 / :68; naive :45),
+    // walking the row backwards so its first reads hit the lines pass 1
+    // (online, naive) read last.
     if constexpr (ALG == osmx_host::kNaive) {
-      map_seg<BLOCK, U>(s, yr, t, [&](float v) { return (float)((double)expf(v) * rd); });
+      map_seg<BLOCK, U>(s, yr, t, [&](float v) { return (float)((double)expf(v) * rd); },
+                        std::integral_constant<bool, true>{});
+    } else if constexpr (ALG == osmx_host::kOnline) {
+      map_seg<BLOCK, U>(s, yr, t, [&](float v) { return expf(v - M) * r; }, std::integral_constant<bool, true>{});
     } else {
       map_seg<BLOCK, U>(s, yr, t, [&](float v) { return expf(v - M) * r; });
     }
@@ -493,14 +498,17 @@ __global__ void __launch_bounds__(BLOCK)
     bad = !(d == d) || !isfinite(M) || mn == kNegInf;
   }
   if (bad && t == 0 && blockIdx.x == 0) flag_bad_row(ws, row);
-  const long long c0 = (long long)blockIdx.x * chunk;
+  // chunks in reverse order: the first CTAs re-read the chunks the part
+  // kernel read last (still in L2 when the row is larger than L2)
+  const long long c0 = (long long)(S - 1 - blockIdx.x) * chunk;
   const long long n = std::min(chunk, V - c0);
   const Seg s = make_seg(x + row * ldx + c0, n);
   float* yr = y + row * ldy + c0;
   if constexpr (ALG == osmx_host::kNaive) {
-    map_seg<BLOCK, U>(s, yr, t, [&](float v) { return (float)((double)expf(v) * rd); });
+    map_seg<BLOCK, U>(s, yr, t, [&](float v) { return (float)((double)expf(v) * rd); },
+                      std::integral_constant<bool, true>{});
   } else {
-    map_seg<BLOCK, U>(s, yr, t, [&](float v) { return expf(v - M) * r; });
+    map_seg<BLOCK, U>(s, yr, t, [&](float v) { return expf(v - M) * r; }, std::integral_constant<bool, true>{});
   }
 }
 
@@ -610,8 +618,9 @@ constexpr int kSplitU = 4;
 long long split_chunk(long long rows, long long V) {
   long long ch = osmx_host::tuning().split_chunk;
   if (ch <= 0) {
-    // ~4 CTAs per SM over the whole problem, at least 32K elements each.
-    const long long target = 4LL * osmx_host::num_sms();
+    // ~14 CTAs per SM over the whole problem (3.5 waves of 512-thread CTAs;
+    // measured on configs[4], tools/c5_sweep.py), at least 32K elements each.
+    const long long target = 14LL * osmx_host::num_sms();
     long long per_row = std::max<long long>(1, target / std::max<long long>(rows, 1));
     ch = (V + per_row - 1) / per_row;
     ch = std::max<long long>(ch, 32768);

@@ -11,6 +11,8 @@
 // needs to reproduce the reference's tie order (topk.hpp:34-44).
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace osmx_dev {
@@ -173,13 +175,61 @@ __device__ __forceinline__ void stream_seg_pipe(const Seg& s, int t, F1&& f1, FB
 // Same traversal, writing one output per element (y has the same alignment
 // phase as x only when ldx == ldy; the output pointer is aligned
 // independently, falling back to scalar stores when phases differ).
-template <int G, int U, class FMAP>
-__device__ __forceinline__ void map_seg(const Seg& s, float* __restrict__ y, int t, FMAP&& f) {
+//
+// REV = true walks the body from its end: the final pass of a multi-pass
+// kernel then starts with the lines the previous pass read last -- still in
+// L2 when the row (or the grid's working set) is larger than L2.
+template <int G, int U, class FMAP, bool REV = false>
+__device__ __forceinline__ void map_seg(const Seg& s, float* __restrict__ y, int t, FMAP&& f,
+                                        std::integral_constant<bool, REV> = {}) {
   const bool same_phase =
       ((reinterpret_cast<uintptr_t>(y) & 15u) == (reinterpret_cast<uintptr_t>(s.p) & 15u));
   if (t < s.head) st_f1(y + t, f(ld_f1_last(s.p + t)));
   const float* b = s.p + s.head;
   float* yb = y + s.head;
+  if constexpr (REV) {
+    // batches of U*G float4s from the last (possibly partial) one down
+    constexpr long long kB = (long long)U * G;
+    const long long nfull = s.nvec / kB;
+    auto one = [&](long long q) {
+      const float4 v = ld_f4_last(b + 4 * q);
+      const float4 o = make_float4(f(v.x), f(v.y), f(v.z), f(v.w));
+      float* dst = yb + 4 * q;
+      if (same_phase) {
+        st_f4(dst, o);
+      } else {
+        st_f1(dst, o.x);
+        st_f1(dst + 1, o.y);
+        st_f1(dst + 2, o.z);
+        st_f1(dst + 3, o.w);
+      }
+    };
+    for (long long q = nfull * kB + t; q < s.nvec; q += G) one(q);  // partial last batch
+    for (long long bi = nfull - 1; bi >= 0; --bi) {
+      float4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = ld_f4_last(b + 4 * (bi * kB + (long long)u * G + t));
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const long long q = bi * kB + (long long)u * G + t;
+        float4 o = make_float4(f(v[u].x), f(v[u].y), f(v[u].z), f(v[u].w));
+        float* dst = yb + 4 * q;
+        if (same_phase) {
+          st_f4(dst, o);
+        } else {
+          st_f1(dst, o.x);
+          st_f1(dst + 1, o.y);
+          st_f1(dst + 2, o.z);
+          st_f1(dst + 3, o.w);
+        }
+      }
+    }
+    if (t < s.tail) {
+      const long long j = s.head + 4 * s.nvec + t;
+      st_f1(y + j, f(ld_f1_last(s.p + j)));
+    }
+    return;
+  }
   long long q = t;
   for (; q + (long long)(U - 1) * G < s.nvec; q += (long long)U * G) {
     float4 v[U];

@@ -18,7 +18,10 @@ size_t record_bytes(int k) { return rec_bytes_(k); }
 size_t topk_split_ws(int alg, long long rows, long long V, int k) {
   const long long ch = topk_split_chunk(rows, V);
   const long long S = (V + ch - 1) / ch;
-  size_t b = (size_t)(rows * S) * rec_bytes_(k);
+  const long long pc = topk_piece_chunk(rows, V);
+  const long long R = (V + pc - 1) / pc;  // warp-per-piece records (fused / topk_of)
+  // + the first-level records of the two-level combine (R >= 1024)
+  size_t b = (size_t)(rows * std::max(S, R + (R + 255) / 256)) * rec_bytes_(k);
   if (alg == kSafeFusedTopk) b += ((size_t)(rows * S) * sizeof(SRecView) + 255) / 256 * 256;
   return b;
 }

@@ -241,10 +241,17 @@ __device__ __forceinline__ void cta_merge(TopList<KC>& L, int k, float* sv, int*
 // BLOCK: CTA per row).  Rows are visited grid-stride.
 // NST > 0 (warp per row only): the body streams through a per-warp
 // cp.async shared-memory pipeline of NST stages (stream_seg_pipe).
+//
+// Record mode (rec != nullptr; fused and topk_of): "rows" are pieces of R
+// per input row -- piece s covers columns [r*chunk, min(V, (r+1)*chunk)) of
+// input row s / R, r = s % R -- and each piece writes a split record (m, d,
+// min, k raw candidates with global column indices + col0) instead of final
+// outputs; k_topk_combine_cta merges the R records of a row.
 template <int G, int BLOCK, int KC, int MODE, int U, int MINB, int NST = 0>
 __global__ void __launch_bounds__(BLOCK, MINB)
     k_topk_rows(const float* __restrict__ x, long long ldx, long long rows, long long V, int k,
-                float* __restrict__ vals, long long* __restrict__ idx, void* ws, int pf) {
+                float* __restrict__ vals, long long* __restrict__ idx, void* ws, int pf, int R = 0,
+                long long chunk = 0, long long col0 = 0, char* __restrict__ rec = nullptr) {
   constexpr int NW = BLOCK / 32;
   constexpr int RPC = BLOCK / G;
   static_assert(NST == 0 || G == 32, "the cp.async pipeline is per warp");
@@ -264,7 +271,15 @@ __global__ void __launch_bounds__(BLOCK, MINB)
     if (G == BLOCK && threadIdx.x == 0) tsh[(it + 1) & 1] = Pass<KC, U, MODE, G>::f2o(kNegInf);
     const long long row = rg * RPC + threadIdx.x / G;
     const bool live = row < rows;
-    const Seg s = make_seg(x + (live ? row : 0) * ldx, live ? V : 0);
+    long long piece0 = 0;  // record mode: first column of this piece
+    Seg s;
+    if (rec) {
+      const long long ir = live ? row / R : 0;
+      piece0 = live ? (row % R) * chunk : 0;
+      s = make_seg(x + ir * ldx + piece0, live ? std::min(chunk, V - piece0) : 0);
+    } else {
+      s = make_seg(x + (live ? row : 0) * ldx, live ? V : 0);
+    }
     Pass<KC, U, MODE, G> P;
     P.L.init(k);
     P.kk = k;
@@ -299,6 +314,7 @@ __global__ void __launch_bounds__(BLOCK, MINB)
     } else {
       run_pass<G, U, KC, MODE>(P, s, t, k, pf);
     }
+    RecHdr hdr{kNegInf, 0.0f, 0.0f, k};
     if constexpr (MODE == kModeFused) {
       MD tot;
       float MN;
@@ -312,6 +328,7 @@ __global__ void __launch_bounds__(BLOCK, MINB)
       outM = tot.m;
       outR = __frcp_rn(tot.d);
       bad = !(tot.d == tot.d) || !isfinite(tot.m) || MN == kNegInf;
+      hdr = RecHdr{tot.m, tot.d, MN, k};
     } else if constexpr (MODE == kModeTopkOf) {
       float c;
       if constexpr (G == 32)
@@ -319,9 +336,16 @@ __global__ void __launch_bounds__(BLOCK, MINB)
       else
         c = cta_sum<NW>(P.chk, smf);
       bad = !(c == c);
+      hdr.mn = (c == c) ? 0.0f : c;
     }
+    char* my = rec && live ? rec + (size_t)row * rec_bytes_(k) : nullptr;
     auto sink = [&](int r, float v, int i) {
       if (live && (int)(threadIdx.x & 31) == (r & 31)) {
+        if (my) {
+          reinterpret_cast<float*>(my + rec_vals_off())[r] = v;
+          reinterpret_cast<long long*>(my + rec_idx_off(k))[r] = i < 0 ? -1LL : (long long)i + piece0 + col0;
+          return;
+        }
         float out = v;
         if constexpr (MODE == kModeFused) out = expf(v - outM) * outR;  // kernels.hpp:122
         vals[row * k + r] = out;
@@ -334,7 +358,11 @@ __global__ void __launch_bounds__(BLOCK, MINB)
     } else {
       cta_merge<NW>(P.L, k, sv, si, sink);
     }
-    if (live && bad && t == 0) flag_bad_row(ws, row);
+    if (my) {
+      if (t == 0) *reinterpret_cast<RecHdr*>(my) = hdr;  // non-finite rows: flagged by the combine
+    } else if (live && bad && t == 0) {
+      flag_bad_row(ws, row);
+    }
   }
 }
 
@@ -471,6 +499,107 @@ __global__ void __launch_bounds__(32)
   }
 }
 
+// CTA-wide combine of the n records of a row (NT threads; for rows split
+// into many pieces): thread t merges records t, t+NT, ... (Eq. 4 merge and
+// the (value desc, index asc) list), then the CTA reduces.  Same outputs as
+// k_topk_combine.
+//
+// Two-level use: grid.y = G > 1 splits each row's records into G groups;
+// CTA (row, g) merges its group into record g of the row in out_rec (no
+// final outputs), and a second launch merges the G records.
+// Each thread sees its records in increasing column order and each record
+// in (value desc, index asc) order, so equal values reach a thread's list
+// in increasing index order and the cheap strict-'>' insertion keeps the
+// reference's tie order; the warp / CTA merges use the full order.
+template <int KC, int NT>
+__global__ void __launch_bounds__(NT)
+    k_topk_combine_cta(const char* __restrict__ rec, int n, int k, int mode, char* __restrict__ out_rec,
+                       float* __restrict__ vals, long long* __restrict__ idx, long long row_base, void* ws) {
+  constexpr int NW = NT / 32;
+  __shared__ float smf[2 * NW];
+  __shared__ float sv[NW * KC];
+  __shared__ long long si[NW * KC];
+  const long long row = blockIdx.x;
+  const int t = threadIdx.x, l = t & 31, w = t >> 5;
+  const size_t rb = rec_bytes_(k);
+  const int G = gridDim.y, g = blockIdx.y;
+  const int per = (n + G - 1) / G;
+  const int c0 = g * per, c1 = min(n, c0 + per);
+  const char* rr = rec + ((size_t)row * n + c0) * rb;
+  n = c1 > c0 ? c1 - c0 : 0;
+  MD a = md_identity();
+  float mn = -kNegInf;
+  float nan_seen = 0.0f;
+  TopList<KC, long long> L;
+  L.init(k);
+  for (int c = t; c < n; c += NT) {
+    // every field of the record is loaded before any is used (independent
+    // loads in flight together; the offers below branch)
+    const char* my = rr + (size_t)c * rb;
+    const RecHdr h = *reinterpret_cast<const RecHdr*>(my);
+    const float* rv = reinterpret_cast<const float*>(my + rec_vals_off());
+    const long long* ri = reinterpret_cast<const long long*>(my + rec_idx_off(k));
+    float cv[KC];
+    long long ci[KC];
+#pragma unroll
+    for (int r = 0; r < KC; ++r) {
+      cv[r] = r < k ? rv[r] : kNegInf;
+      ci[r] = r < k ? ri[r] : -1LL;
+    }
+    a = md_merge(a, MD{h.m, h.d});
+    if (h.mn != h.mn) nan_seen = 1.0f;
+    mn = fminf(mn, h.mn);
+#pragma unroll
+    for (int r = 0; r < KC; ++r)
+      if (r < k) L.offer(cv[r], ci[r]);
+  }
+  a = md_cta_reduce<NW>(a, smf);
+  mn = cta_min<NW>(mn, smf);
+  nan_seen = cta_sum<NW>(nan_seen, smf);
+  bool bad;
+  if (mode == kModeFused)
+    bad = !(a.d == a.d) || !isfinite(a.m) || mn == kNegInf || nan_seen > 0.0f;
+  else
+    bad = nan_seen > 0.0f;
+  const float R = __frcp_rn(a.d);
+  char* orec = out_rec ? out_rec + ((size_t)row * G + g) * rb : nullptr;
+  if (G > 1) vals = nullptr, bad = false;  // first level: records only
+  // per-warp k winners -> shared memory -> warp 0 merges NW * k candidates
+  L.normalize(k);
+  group_merge<32>(L, k, [&](int r, float v, long long i) {
+    if (l == 0) {
+      sv[w * KC + r] = v;
+      si[w * KC + r] = i;
+    }
+  });
+  __syncthreads();
+  if (w == 0) {
+    TopList<KC, long long> M;
+    M.init(k);
+    for (int q = l; q < NW * k; q += 32) {
+      const int ww = q / k, r = q % k;
+      M.offer_ordered(sv[ww * KC + r], si[ww * KC + r]);
+    }
+    M.normalize(k);
+    group_merge<32>(M, k, [&](int r, float v, long long i) {
+      if (l == (r & 31)) {
+        if (orec) {
+          reinterpret_cast<float*>(orec + rec_vals_off())[r] = v;
+          reinterpret_cast<long long*>(orec + rec_idx_off(k))[r] = i;
+        }
+        if (vals) {
+          vals[row * k + r] = mode == kModeFused ? expf(v - a.m) * R : v;
+          idx[row * k + r] = i;
+        }
+      }
+    });
+    if (l == 0) {
+      if (orec) *reinterpret_cast<RecHdr*>(orec) = RecHdr{a.m, a.d, nan_seen > 0.0f ? __int_as_float(0x7fffffff) : mn, k};
+      if (bad && ws) flag_bad_row(ws, row_base + row);
+    }
+  }
+}
+
 // ------------------------------------------------------------ launchers --
 
 // Threads per row: enough rows in flight to fill every SM several times,
@@ -554,6 +683,18 @@ long long topk_split_chunk(long long rows, long long V) {
   return (ch + 15) / 16 * 16;
 }
 
+// Piece length of the warp-per-piece split path: about one wave of warps
+// (28 per SM) over the whole problem, 8K..64K elements, a multiple of 16.
+long long topk_piece_chunk(long long rows, long long V) {
+  long long ch = osmx_host::tuning().split_chunk;
+  if (ch <= 0) {
+    const long long waves = 28LL * osmx_host::num_sms();
+    ch = (rows * V + waves - 1) / waves;
+    ch = std::min<long long>(std::max<long long>(ch, 8192), 65536);
+  }
+  return (ch + 15) / 16 * 16;
+}
+
 template <int KC, int MODE>
 cudaError_t run_split(const float* x, long long ldx, long long rows, long long V, int k, float* vals,
                       long long* idx, void* ws, cudaStream_t st, long long col0, char* out_rec) {
@@ -568,6 +709,40 @@ cudaError_t run_split(const float* x, long long ldx, long long rows, long long V
     rec = base + ((size_t)(rows * S) * sizeof(SRecView) + 255) / 256 * 256;
     cudaError_t e = osmx_host::launch_safe_split_stats(x, ldx, rows, V, ch, const_cast<SRecView*>(srec), st);
     if (e != cudaSuccess) return e;
+  }
+  if constexpr (MODE != kModeSafe) {
+    if (osmx_host::tuning().split_cta == 0) {
+      // Warp-per-piece records (the warp-per-row kernel in record mode: one
+      // ~16K-element piece per warp, about one wave of warps over the whole
+      // problem), then a CTA-wide combine per row.
+      const long long pc = topk_piece_chunk(rows, V);
+      const long long R = (V + pc - 1) / pc;
+      const long long pieces = rows * R;
+      if (pieces <= 28LL * osmx_host::num_sms() && pc >= 8192) {
+        const long long grid = (pieces + 3) / 4;
+        k_topk_rows<32, 128, KC, MODE, 8, 7><<<(unsigned)grid, 128, 0, st>>>(x, ldx, pieces, V, k, nullptr, nullptr,
+                                                                          ws, 0, (int)R, pc, col0, rec);
+      } else {
+        const long long grid = std::min<long long>((pieces + 7) / 8, 1LL << 30);
+        k_topk_rows<32, 256, KC, MODE, 4, 4><<<(unsigned)grid, 256, 0, st>>>(x, ldx, pieces, V, k, nullptr, nullptr,
+                                                                          ws, 0, (int)R, pc, col0, rec);
+      }
+      osmx_host::count_launch();
+      if (R >= 1024) {
+        // two levels: G groups of <= 256 records per row, then the G records
+        const int G = (int)((R + 255) / 256);
+        char* mid = rec + (size_t)(rows * R) * rec_bytes_(k);
+        k_topk_combine_cta<KC, 256><<<dim3((unsigned)rows, (unsigned)G), 256, 0, st>>>(rec, (int)R, k, MODE, mid,
+                                                                                    nullptr, nullptr, 0, ws);
+        k_topk_combine_cta<KC, 256><<<(unsigned)rows, 256, 0, st>>>(mid, G, k, MODE, out_rec, vals, idx, 0, ws);
+        osmx_host::count_launch();
+      } else if (R >= 64) {
+        k_topk_combine_cta<KC, 256><<<(unsigned)rows, 256, 0, st>>>(rec, (int)R, k, MODE, out_rec, vals, idx, 0, ws);
+      } else
+        k_topk_combine<KC><<<(unsigned)rows, 32, 0, st>>>(rec, (int)R, k, MODE, out_rec, vals, idx, 0, ws);
+      osmx_host::count_launch();
+      return cudaGetLastError();
+    }
   }
   dim3 grid((unsigned)S, (unsigned)rows);
   k_topk_split_part<kSplitBlock, KC, MODE, kSplitU><<<grid, kSplitBlock, 0, st>>>(x, ldx, V, ch, k, col0, rec, srec);

@@ -25,6 +25,8 @@ TOPK_VARIANTS = {
     "warp_pf": [("topk_threads", 32), ("l2_prefetch", 2)], "cta_pf": [("topk_threads", 256), ("l2_prefetch", 1)],
     "warp_pipe1": [("topk_threads", 32), ("topk_pipe", 1)], "warp_pipe2": [("topk_threads", 32), ("topk_pipe", 2)],
     "warp_pipe3": [("topk_threads", 32), ("topk_pipe", 3)],
+    "split_cta": [("shape", 3), ("split_chunk", 2048), ("split_cta", 1)],
+    "split_auto": [("shape", 3)],
 }
 
 
@@ -35,7 +37,7 @@ def lib():
     _lib.load()
     yield _lib
     for key, val in (("shape", 0), ("split_chunk", 0), ("tma", 0), ("topk_threads", 0), ("topk_u8", -1),
-                     ("l2_prefetch", 0), ("cluster_size", 0), ("topk_pipe", 0)):
+                     ("l2_prefetch", 0), ("cluster_size", 0), ("topk_pipe", 0), ("split_cta", 0)):
         _lib.config_set(key, val)
 
 
