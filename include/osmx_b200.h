@@ -43,7 +43,8 @@ typedef enum {
   OSMX_ERR_INVALID_CHUNK = 4, /* invalid_chunk_error error.hpp:23-25 */
   OSMX_ERR_INVALID_ARG = 5,   /* null pointer, ld < V, bad enum, ws too small */
   OSMX_ERR_CUDA = 6,          /* a CUDA runtime error (see osmx_last_cuda_error) */
-  OSMX_ERR_UNSUPPORTED = 7    /* k above OSMX_MAX_K on the device path */
+  OSMX_ERR_UNSUPPORTED = 7    /* split / slice records with k > OSMX_MAX_K; top-K with
+                                 V >= 2^31 or rows * k >= 2^31 when k > OSMX_MAX_K */
 } osmx_status;
 
 /* Algorithm ids: the reference's `algorithm` enum order (counting.hpp:17-24)
@@ -58,6 +59,10 @@ typedef enum {
   OSMX_ONLINE_SOFTMAX_UNFUSED_TOPK = 6  /* online_softmax then topk_of (new) */
 } osmx_algorithm;
 
+/* Largest k of the fused register top-K lists and of the fixed-size split /
+ * slice records.  Top-K calls accept any 1 <= k <= V (the reference's
+ * contract, kernels.hpp:28-30); k > OSMX_MAX_K takes the radix-select path
+ * (csrc/topk_large.cu), whose workspace grows with rows * k. */
 #define OSMX_MAX_K 32
 #define OSMX_VERSION 100
 

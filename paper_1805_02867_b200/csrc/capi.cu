@@ -59,7 +59,8 @@ static size_t split_region(int alg, long long rows, long long V, int k) {
       break;
     case kSafeFusedTopk:
     case kOnlineFusedTopk:
-      if (topk_split(rows, V)) b = topk_split_ws(alg, rows, V, k);
+      if (k > kMaxK) b = topk_large_ws(rows, V, k);
+      else if (topk_split(rows, V)) b = topk_split_ws(alg, rows, V, k);
       break;
     case kSliceRecord:  // always the split path (piece records + combine)
       b = topk_split_ws(kOnlineFusedTopk, rows, V, k);
@@ -68,7 +69,8 @@ static size_t split_region(int alg, long long rows, long long V, int k) {
     case kOnlineUnfusedTopk:
     case kTopkOf: {
       if (softmax_uses_split(rows, V)) b = std::max(b, softmax_split_ws(rows, V));
-      if (topk_split(rows, V)) b = std::max(b, topk_split_ws(kTopkOf, rows, V, k));
+      if (k > kMaxK) b = std::max(b, topk_large_ws(rows, V, k));
+      else if (topk_split(rows, V)) b = std::max(b, topk_split_ws(kTopkOf, rows, V, k));
       break;
     }
     default:
@@ -110,9 +112,9 @@ osmx_status check_common(const void* x, long long ld, long long rows, long long 
   return OSMX_OK;
 }
 
-osmx_status check_k(long long V, int k) {
+osmx_status check_k(long long V, int k, long long rows = 1) {
   if (k < 1 || (long long)k > V) return OSMX_ERR_INVALID_K;  // require_valid_k, kernels.hpp:28-30
-  if (k > kMaxK) return OSMX_ERR_UNSUPPORTED;
+  if (k > kMaxK && !topk_large_supported(rows, V, k)) return OSMX_ERR_UNSUPPORTED;
   return OSMX_OK;
 }
 
@@ -155,7 +157,7 @@ const char* osmx_status_string(osmx_status s) {
     case OSMX_ERR_INVALID_CHUNK: return "chunk length must be >= 1";
     case OSMX_ERR_INVALID_ARG: return "invalid argument";
     case OSMX_ERR_CUDA: return "CUDA error";
-    case OSMX_ERR_UNSUPPORTED: return "unsupported (k above OSMX_MAX_K)";
+    case OSMX_ERR_UNSUPPORTED: return "unsupported (records: k above OSMX_MAX_K; large k: rows * k >= 2^31)";
   }
   return "unknown status";
 }
@@ -201,7 +203,7 @@ osmx_status osmx_softmax_topk(int alg, const float* x, int64_t ldx, int64_t rows
   if (!is_topk(alg)) return OSMX_ERR_INVALID_ARG;
   osmx_status s = check_common(x, ldx, rows, V);
   if (s) return s;
-  if ((s = check_k(V, k))) return s;
+  if ((s = check_k(V, k, rows))) return s;
   if ((rows > 0 && (!vals || !idx)) || !ws) return OSMX_ERR_INVALID_ARG;
   if (rows == 0) return OSMX_OK;
   if (ws_bytes < workspace_bytes(alg, rows, V, k)) return OSMX_ERR_INVALID_ARG;
@@ -213,7 +215,7 @@ osmx_status osmx_topk(const float* v, int64_t ld, int64_t rows, int64_t V, int32
                       void* ws, size_t ws_bytes, void* stream) {
   osmx_status s = check_common(v, ld, rows, V);
   if (s) return s;
-  if ((s = check_k(V, k))) return s;
+  if ((s = check_k(V, k, rows))) return s;
   if ((rows > 0 && (!vals || !idx)) || !ws) return OSMX_ERR_INVALID_ARG;
   if (rows == 0) return OSMX_OK;
   if (ws_bytes < workspace_bytes(kTopkOf, rows, V, k)) return OSMX_ERR_INVALID_ARG;

@@ -100,7 +100,14 @@ bool topk_split(long long rows, long long V);
 cudaError_t launch_topk_mode(int mode, const float* x, long long ldx, long long rows, long long V,
                              int k, float* vals, long long* idx, void* ws, cudaStream_t st);
 
-// Largest k served by the register top-K lists.
+// Largest k served by the register top-K lists (and by split records).
 constexpr int kMaxK = 32;
+
+// topk_large.cu: any k above kMaxK (radix select + ordered compaction +
+// stable segmented sort).  region = workspace after the header.
+size_t topk_large_ws(long long rows, long long V, int k);
+bool topk_large_supported(long long rows, long long V, int k);
+cudaError_t launch_topk_large(int mode, const float* x, long long ldx, long long rows, long long V, int k,
+                              float* vals, long long* idx, void* ws, void* region, cudaStream_t st);
 
 }  // namespace osmx_host

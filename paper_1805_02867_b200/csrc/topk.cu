@@ -40,6 +40,8 @@ bool topk_uses_tma(int mode, long long rows, long long V) {
 
 cudaError_t launch_topk_mode(int mode, const float* x, long long ldx, long long rows, long long V, int k,
                              float* vals, long long* idx, void* ws, cudaStream_t st) {
+  if (k > kMaxK)
+    return launch_topk_large(mode, x, ldx, rows, V, k, vals, idx, ws, static_cast<char*>(ws) + kWsHeader, st);
   const bool split = topk_uses_split(rows, V);
   if (topk_uses_tma(mode, rows, V)) return launch_topk_tma(mode, x, ldx, rows, V, k, vals, idx, ws, st);
   switch (mode) {

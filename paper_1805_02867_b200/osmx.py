@@ -97,7 +97,8 @@ def _raise(status: int, row: int = -1) -> None:
     if status == _lib.ERR_CUDA:
         raise CudaError(load().osmx_last_cuda_error().decode())
     if status == _lib.ERR_UNSUPPORTED:
-        raise UnsupportedError(f"k above {_lib.MAX_K} is not supported on the device path")
+        raise UnsupportedError(f"unsupported on the device path (records need k <= {_lib.MAX_K}; "
+                               "large-k top-K needs rows * k < 2^31)")
     raise ValueError(_lib.status_string(status))
 
 

@@ -73,8 +73,10 @@ def test_validation_without_gpu():
     assert lib.osmx_softmax_topk(5, fake, 10, 4, 10, 0, fake, fake, ws, 1 << 20, None) == _lib.ERR_INVALID_K
     assert lib.osmx_softmax_topk(5, fake, 10, 4, 10, 11, fake, fake, ws, 1 << 20, None) == _lib.ERR_INVALID_K
     assert lib.osmx_topk(fake, 10, 4, 10, 11, fake, fake, ws, 1 << 20, None) == _lib.ERR_INVALID_K
-    # device path limit for k
-    assert lib.osmx_softmax_topk(5, fake, 100, 4, 100, 33, fake, fake, ws, 1 << 20, None) == _lib.ERR_UNSUPPORTED
+    # device path limits: large-k top-K needs rows * k < 2^31; records k <= OSMX_MAX_K
+    assert lib.osmx_softmax_topk(5, fake, 4096, 1 << 20, 4096, 4096, fake, fake, ws, 1 << 20,
+                                 None) == _lib.ERR_UNSUPPORTED
+    assert lib.osmx_slice_record(fake, 100, 0, 33, fake, ws, 1 << 20, None) == _lib.ERR_UNSUPPORTED
     # bad algorithm id / ld < V / null pointers / small workspace
     assert lib.osmx_softmax(9, fake, 10, fake, 10, 4, 10, ws, 1 << 20, None) == _lib.ERR_INVALID_ARG
     assert lib.osmx_softmax(2, fake, 5, fake, 10, 4, 10, ws, 1 << 20, None) == _lib.ERR_INVALID_ARG

@@ -312,8 +312,8 @@ def test_argument_errors(cuda, lib):
         osmx.softmax_topk(x, 0)
     with pytest.raises(osmx.InvalidKError):
         osmx.softmax_topk(x, 5)
-    with pytest.raises(osmx.UnsupportedError):
-        osmx.softmax_topk(_dev(np.zeros((1, 100), np.float32)), 33)
+    with pytest.raises(osmx.InvalidKError):
+        osmx.softmax_topk(_dev(np.zeros((1, 100), np.float32)), 101)
     with pytest.raises(osmx.EmptyInputError):
         osmx.softmax(_dev(np.zeros((2, 0), np.float32)))
 
@@ -369,3 +369,33 @@ def test_softmax_cluster_slices(cuda, oracle_mod, lib, alg):
             ref, st = oracle_mod.batch(f"{alg}_softmax", x)
             assert (st == 0).all()
             assert max_rel(y, ref) <= TOL, (alg, V, C, d)
+
+
+@pytest.mark.parametrize("k", [33, 100, 1000, "V"])
+def test_large_k(cuda, oracle_mod, lib, k):
+    """k above the register lists (radix select + ordered compaction + stable
+    segmented sort): indices bit-exact for the raw-key modes, probability
+    collisions only for the probability-key modes; k = V sorts whole rows."""
+    from paper_1805_02867_b200 import osmx
+
+    rng = np.random.default_rng(500)
+    for V in (1000, 4099, 70001):
+        kk = V if k == "V" else min(int(k), V)
+        if kk == V and V > 5000:
+            continue
+        for d in ("normal", "quantized2", "equal", "descending", "spikes"):
+            x = dist(d, rng, 4, V)
+            vals, idx = osmx.softmax_topk(_dev(x), kk, alg="online_fused")
+            rv, rz = _topk_ref(oracle_mod, "online_softmax_topk", x, kk)
+            assert np.array_equal(idx.cpu().numpy(), rz), (V, kk, d)
+            assert max_rel(vals.cpu().numpy(), rv) <= TOL
+            tv, ti = osmx.topk(_dev(x), kk)
+            rv, rz = _topk_ref(oracle_mod, "topk_of", x, kk)
+            assert np.array_equal(ti.cpu().numpy(), rz), (V, kk, d)
+            assert np.array_equal(tv.cpu().numpy().view(np.int32), rv.view(np.int32))
+            for alg, op in (("safe_fused", "safe_softmax_fused_topk"), ("safe_unfused", "safe_softmax_then_topk")):
+                vals, idx = osmx.softmax_topk(_dev(x), kk, alg=alg)
+                y, _ = oracle_mod.batch("safe_softmax", x)
+                rv, rz = _topk_ref(oracle_mod, op, x, kk)
+                _prob_collisions(idx.cpu().numpy(), rz, lambda r: y[r])
+                assert max_rel(vals.cpu().numpy(), rv) <= TOL
