@@ -16,7 +16,7 @@ HDRS = $(wildcard $(SRC_DIR)/*.cuh) $(SRC_DIR)/internal.hpp include/osmx_b200.h
 OBJS = $(patsubst $(SRC_DIR)/%.cu,build/%.o,$(SRCS))
 LIB = paper_1805_02867_b200/libosmx_b200.so
 
-all: $(LIB) oracle cxxtest
+all: $(LIB) oracle cxxtest benchcli
 
 build/%.o: $(SRC_DIR)/%.cu $(HDRS)
 	@mkdir -p build
@@ -44,3 +44,13 @@ $(CXXTEST): tests/cpp/test_reference_api.cpp include/osmx/b200.hpp include/osmx_
 
 cxxtest: $(CXXTEST)
 .PHONY: cxxtest
+
+# GPU twin of the reference's osmx-bench CLI (same flags / table / count model)
+BENCHCLI = build/osmx-bench-gpu
+$(BENCHCLI): tools/osmx_bench_gpu.cu include/osmx_b200.h $(LIB)
+	@mkdir -p build
+	$(NVCC) $(ARCH) -O2 -std=c++17 -Iinclude -o $@ $< -L paper_1805_02867_b200 -losmx_b200 \
+	    -Xlinker -rpath,'$$ORIGIN/../paper_1805_02867_b200'
+
+benchcli: $(BENCHCLI)
+.PHONY: benchcli
