@@ -529,6 +529,26 @@ def n_rotating_sets(set_bytes: int, l2: int, cap_bytes: int = 48 << 30) -> int:
     return int(max(2, min(n, cap_bytes // max(set_bytes, 1))))
 
 
+Vs_all = [10, 18, 32, 56, 100, 178, 316, 562, 1000, 1778, 3162, 5623, 10000, 17783, 31623, 56234, 100000, 177828,
+          316228, 562341, 1000000]  # configs[1]: log_spaced_sizes(10, 1e6, 21)
+Vt_all = [32768, 65536, 131072, 262144, 524288, 1048576]  # configs[2]
+
+
+class Arena:
+    """One float32 device buffer; take(offset, shape) returns views of it."""
+
+    def __init__(self, n_floats: int, dev):
+        import torch
+
+        self.buf = torch.empty(int(n_floats), dtype=torch.float32, device=dev)
+
+    def take(self, off: int, shape):
+        n = 1
+        for d in shape:
+            n *= d
+        return self.buf[off:off + n].view(*shape)
+
+
 def run_sweeps(lib, _lib, dev, sp, reps, peak) -> dict:
     """configs[1]: safe vs online softmax, batch 4000, V = log_spaced(10, 1e6, 21).
     configs[2]: fused online softmax+Top-5 vs unfused online->TopK, batch 4000,
@@ -540,15 +560,22 @@ def run_sweeps(lib, _lib, dev, sp, reps, peak) -> dict:
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     B = 4000
     k = K_TOP
+    # One arena for every buffer of the sweep, allocated once: the physical
+    # mapping of a buffer allocated after large frees can cost the latency-
+    # bound fused top-K ~25% (tools/placement_test.py), so all sizes share
+    # one mapping instead of each getting a fresh one.
+    need = max(max(2 * n_rotating_sets(8 * B * V, l2) * B * V for V in Vs_all),
+               max(n_rotating_sets(4 * B * V, l2) * B * V for V in Vt_all), 2 * n_rotating_sets(8 << 26, l2) << 26)
+    arena = Arena(need, dev)
     out = {"batch": B, "k": k, "timing": "CUDA graph of n_sets launches over rotating buffer sets "
-                                          "(>= 4 x L2, inputs cold in L2), CUDA events, median",
+                                          "(>= 4 x L2, inputs cold in L2), CUDA events, median; one "
+                                          "preallocated arena for all buffers",
            "softmax": [], "topk": []}
-    Vs = [10, 18, 32, 56, 100, 178, 316, 562, 1000, 1778, 3162, 5623, 10000, 17783, 31623, 56234, 100000, 177828,
-          316228, 562341, 1000000]
+    Vs = Vs_all
     for V in Vs:
         n = n_rotating_sets(8 * B * V, l2)
-        x = torch.empty((n, B, V), dtype=torch.float32, device=dev).normal_()
-        y = torch.empty_like(x)
+        x = arena.take(0, (n, B, V)).normal_()
+        y = arena.take(n * B * V, (n, B, V))
         row = {"V": V, "n_sets": n}
         # best kernel family per V (auto), and the paper's one-CTA-per-row
         # streaming kernels (shape 2: every pass reads global memory; the
@@ -575,10 +602,9 @@ def run_sweeps(lib, _lib, dev, sp, reps, peak) -> dict:
         row["online_over_safe_stream"] = round(row["safe_stream"]["ms"] / row["online"]["ms"], 3)
         out["softmax"].append(row)
         del x, y
-        torch.cuda.empty_cache()
-    for V in [32768, 65536, 131072, 262144, 524288, 1048576]:
+    for V in Vt_all:
         n = n_rotating_sets(4 * B * V, l2)
-        x = torch.empty((n, B, V), dtype=torch.float32, device=dev).normal_()
+        x = arena.take(0, (n, B, V)).normal_()
         vals = torch.empty((B, k), dtype=torch.float32, device=dev)
         idx = torch.empty((B, k), dtype=torch.int64, device=dev)
         row = {"V": V, "n_sets": n}
@@ -608,12 +634,13 @@ def run_sweeps(lib, _lib, dev, sp, reps, peak) -> dict:
                                                         3)
         out["topk"].append(row)
         del x
-        torch.cuda.empty_cache()
-    out["c5"] = run_c5(lib, _lib, dev, reps, peak, l2)
+    out["c5"] = run_c5(lib, _lib, dev, reps, peak, l2, arena)
+    del arena
+    torch.cuda.empty_cache()
     return out
 
 
-def run_c5(lib, _lib, dev, reps, peak, l2) -> dict:
+def run_c5(lib, _lib, dev, reps, peak, l2, arena=None) -> dict:
     """configs[4] on one GPU: a single row of V = 2^26 (256 MB), fused online
     softmax + Top-5 and online softmax, split over CTAs with the (m, d) /
     top-K record combine (the per-GPU leg of the NCCL V-split)."""
@@ -621,8 +648,10 @@ def run_c5(lib, _lib, dev, reps, peak, l2) -> dict:
 
     V, k = 1 << 26, K_TOP
     n = n_rotating_sets(8 * V, l2)
-    x = torch.empty((n, V), dtype=torch.float32, device=dev).normal_()
-    y = torch.empty_like(x)
+    if arena is None:
+        arena = Arena(2 * n * V, dev)
+    x = arena.take(0, (n, V)).normal_()
+    y = arena.take(n * V, (n, V))
     vals = torch.empty((1, k), dtype=torch.float32, device=dev)
     idx = torch.empty((1, k), dtype=torch.int64, device=dev)
     res = {"rows": 1, "V": V, "k": k, "n_sets": n}
@@ -643,7 +672,6 @@ def run_c5(lib, _lib, dev, reps, peak, l2) -> dict:
         res[name] = {"ms": round(ms, 5), "GBps": round(gbs, 1), "frac": round(gbs / peak, 3),
                      "elements_per_s": round(V / (ms * 1e-3), 1)}
     del x, y
-    torch.cuda.empty_cache()
     return res
 
 
