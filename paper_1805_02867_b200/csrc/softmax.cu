@@ -16,8 +16,9 @@ size_t softmax_split_ws(long long rows, long long V) {
 }
 
 int resident_limit(bool vec) {
+  // unaligned rows span up to V + 3 float4 lanes: keep them in the same shape
   const int r = tuning().resident_max_v;
-  return vec ? r : std::min(r, 4096);
+  return vec ? r : std::min(r, 4096) - 3;
 }
 
 // Conservative (workspace sizing does not know the pointers' alignment).

@@ -134,15 +134,36 @@ __global__ void __launch_bounds__(TPR > 256 ? TPR : 256)
       a[4 * t + 3] = v.w;
     }
   } else {
+    // Rows not 16-byte aligned (V % 4 != 0 or an odd ld / base): float4 q
+    // of the aligned base xr - phase holds elements 4q - phase .. 4q + 3 -
+    // phase; interior float4s load with LDG.128, the <= 2 edge ones
+    // element-wise (only in-row addresses are touched).
+    const int phase = (int)((reinterpret_cast<uintptr_t>(xr) >> 2) & 3);
+    const float* xb = xr - phase;
 #pragma unroll
-    for (int t = 0; t < EPT; ++t) {
-      const int e = g + TPR * t;
-      float v = kNegInf;
-      if (live && e < V) {
-        v = ld_f1(xr + e);
-        bad |= !isfinite(v);
+    for (int t = 0; t < EPT / 4; ++t) {
+      const int q = g + TPR * t;
+      const int e0 = 4 * q - phase;
+      float4 v = make_float4(kNegInf, kNegInf, kNegInf, kNegInf);
+      if (live && e0 < V) {
+        if (e0 >= 0 && e0 + 4 <= V) {
+          v = ld_f4(xb + 4 * q);
+        } else {
+          if (e0 + 0 >= 0 && e0 + 0 < V) v.x = ld_f1(xr + e0 + 0);
+          if (e0 + 1 >= 0 && e0 + 1 < V) v.y = ld_f1(xr + e0 + 1);
+          if (e0 + 2 >= 0 && e0 + 2 < V) v.z = ld_f1(xr + e0 + 2);
+          if (e0 + 3 >= 0 && e0 + 3 < V) v.w = ld_f1(xr + e0 + 3);
+        }
+        // masked lanes hold -inf (never "bad": -inf elements are detected below only if in-row)
+        const bool in0 = e0 + 0 >= 0 && e0 + 0 < V, in1 = e0 + 1 >= 0 && e0 + 1 < V;
+        const bool in2 = e0 + 2 >= 0 && e0 + 2 < V, in3 = e0 + 3 >= 0 && e0 + 3 < V;
+        bad |= (in0 && !isfinite(v.x)) || (in1 && !isfinite(v.y)) || (in2 && !isfinite(v.z)) ||
+               (in3 && !isfinite(v.w));
       }
-      a[t] = v;
+      a[4 * t] = v.x;
+      a[4 * t + 1] = v.y;
+      a[4 * t + 2] = v.z;
+      a[4 * t + 3] = v.w;
     }
   }
 
@@ -209,10 +230,23 @@ __global__ void __launch_bounds__(TPR > 256 ? TPR : 256)
         st_f4(yr + 4 * q, make_float4(f(a[4 * t]), f(a[4 * t + 1]), f(a[4 * t + 2]), f(a[4 * t + 3])));
     }
   } else {
+    const int phase = (int)((reinterpret_cast<uintptr_t>(xr) >> 2) & 3);
+    const bool same = ((reinterpret_cast<uintptr_t>(yr) >> 2) & 3) == (uintptr_t)phase;
+    float* yb = yr - phase;
 #pragma unroll
-    for (int t = 0; t < EPT; ++t) {
-      const int e = g + TPR * t;
-      if (e < V) st_f1(yr + e, f(a[t]));
+    for (int t = 0; t < EPT / 4; ++t) {
+      const int q = g + TPR * t;
+      const int e0 = 4 * q - phase;
+      if (e0 >= V) continue;
+      const float4 o = make_float4(f(a[4 * t]), f(a[4 * t + 1]), f(a[4 * t + 2]), f(a[4 * t + 3]));
+      if (same && e0 >= 0 && e0 + 4 <= V) {
+        st_f4(yb + 4 * q, o);
+      } else {
+        if (e0 + 0 >= 0 && e0 + 0 < V) st_f1(yr + e0 + 0, o.x);
+        if (e0 + 1 >= 0 && e0 + 1 < V) st_f1(yr + e0 + 1, o.y);
+        if (e0 + 2 >= 0 && e0 + 2 < V) st_f1(yr + e0 + 2, o.z);
+        if (e0 + 3 >= 0 && e0 + 3 < V) st_f1(yr + e0 + 3, o.w);
+      }
     }
   }
 }
@@ -572,15 +606,27 @@ cudaError_t run_resident(bool vec, const float* x, long long ldx, float* y, long
 
 template <int ALG>
 cudaError_t dispatch_resident(bool vec, const float* x, long long ldx, float* y, long long ldy,
-                              long long rows, long long V, void* ws, cudaStream_t st) {
-  if (V <= 64) return run_resident<8, 8, ALG>(vec, x, ldx, y, ldy, rows, V, ws, st);
-  if (V <= 256) return run_resident<32, 8, ALG>(vec, x, ldx, y, ldy, rows, V, ws, st);
-  if (V <= 512) return run_resident<32, 16, ALG>(vec, x, ldx, y, ldy, rows, V, ws, st);
-  if (V <= 1024) return run_resident<32, 32, ALG>(vec, x, ldx, y, ldy, rows, V, ws, st);
-  if (V <= 2048) return run_resident<128, 16, ALG>(vec, x, ldx, y, ldy, rows, V, ws, st);
-  if (V <= 4096) return run_resident<256, 16, ALG>(vec, x, ldx, y, ldy, rows, V, ws, st);
-  if (V <= 8192) return run_resident<256, 32, ALG>(vec, x, ldx, y, ldy, rows, V, ws, st);
-  return run_resident<512, 32, ALG>(vec, x, ldx, y, ldy, rows, V, ws, st);
+                              long long rows, long long V_, void* ws, cudaStream_t st) {
+  // shapes by capacity: unaligned rows span up to V + 3 float4 lanes
+  const long long V = vec ? V_ : V_ + 3;
+  auto run = [&](auto tpr, auto ept) {
+    return run_resident<decltype(tpr)::value, decltype(ept)::value, ALG>(vec, x, ldx, y, ldy, rows, V_, ws, st);
+  };
+  using I8 = std::integral_constant<int, 8>;
+  using I16 = std::integral_constant<int, 16>;
+  using I32 = std::integral_constant<int, 32>;
+  using I128 = std::integral_constant<int, 128>;
+  using I256 = std::integral_constant<int, 256>;
+  using I512 = std::integral_constant<int, 512>;
+  if (V <= 64) return run(I8{}, I8{});
+  if (V <= 256) return run(I32{}, I8{});
+  if (V <= 512) return run(I32{}, I16{});
+  if (V <= 1024) return run(I32{}, I32{});
+  if (V <= 2048) return run(I128{}, I16{});
+  if (V <= 4096) return run(I256{}, I16{});
+  if (V <= 8192) return run(I256{}, I32{});
+  if (V <= 16384) return run(I512{}, I32{});
+  return cudaErrorInvalidValue;
 }
 
 template <int ALG>
@@ -671,7 +717,7 @@ cudaError_t launch_alg(const float* x, long long ldx, float* y, long long ldy, l
     else
       shape = osmx_host::kShapeSplit;
   }
-  if (shape == osmx_host::kShapeResident && V > 16384) shape = osmx_host::kShapeStream;
+  if (shape == osmx_host::kShapeResident && V + (vec ? 0 : 3) > 16384) shape = osmx_host::kShapeStream;
   if (shape == osmx_host::kShapeStaged || shape == osmx_host::kShapeCluster) {
     if (V <= kClusterMaxV || osmx_host::tuning().cluster_size > 0) return run_staged<ALG>(x, ldx, y, ldy, rows, V, ws, st);
     shape = osmx_host::kShapeStream;
