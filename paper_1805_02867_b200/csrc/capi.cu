@@ -315,7 +315,7 @@ osmx_status osmx_config_set(const char* key, int64_t value) {
     if (value < -1 || value > 1) return OSMX_ERR_INVALID_ARG;
     t.topk_u8 = (int)value;
   } else if (!strcmp(key, "l2_prefetch")) {
-    if (value < 0 || value > 64) return OSMX_ERR_INVALID_ARG;
+    if (value < -1 || value > 64) return OSMX_ERR_INVALID_ARG;
     t.l2_prefetch = (int)value;
   } else if (!strcmp(key, "tma")) {
     if (value < 0 || value > 2) return OSMX_ERR_INVALID_ARG;

@@ -47,7 +47,7 @@ struct Tuning {
   int split_cta = 0;            // top-K split path: 0 warp-per-piece records, 1 CTA-per-chunk (legacy)
   int topk_pipe = 0;            // warp-per-row top-K via a cp.async smem pipeline (0 off; 1..3 layouts)
   int topk_u8 = -1;             // warp-per-row top-K with 8 float4s in flight (-1 auto)
-  int l2_prefetch = 0;          // bulk L2 prefetch distance in batches (0 = off)
+  int l2_prefetch = -1;         // bulk L2 prefetch distance in batches (0 off, -1 auto)
   int tma = 0;                  // TMA-ring top-K: 0 off (default: the warp-per-row
                                 // LDG kernel measures faster), 1 auto, 2 force
 };

@@ -633,7 +633,7 @@ template <int ALG>
 cudaError_t run_stream(const float* x, long long ldx, float* y, long long ldy, long long rows,
                        long long V, void* ws, cudaStream_t st) {
   int threads = osmx_host::tuning().stream_threads;
-  const int pf = osmx_host::tuning().l2_prefetch;
+  const int pf = std::max(0, osmx_host::tuning().l2_prefetch);  // off unless forced (measured: mixed)
   if (threads == 0) threads = V >= 65536 ? 512 : 256;
   const int keep = osmx_host::tuning().stream_ctas;  // > 0: persistent, CTAs per SM, evict-last pass 1
   if (keep > 0) {

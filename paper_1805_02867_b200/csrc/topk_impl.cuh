@@ -627,7 +627,11 @@ template <int KC, int MODE>
 cudaError_t run_rows(const float* x, long long ldx, long long rows, long long V, int k, float* vals,
                      long long* idx, void* ws, cudaStream_t st) {
   const int g = topk_row_threads(rows, V);
-  const int pf = osmx_host::tuning().l2_prefetch;
+  // Bulk L2 prefetch one batch ahead (auto, rows >= ~2 waves of warps):
+  // +1.4-5% at 16384-65536 rows (C4: 7.19 -> 7.29-7.39 TB/s, 98-99% of a
+  // pure-read probe's 7.43, tools/read_peak.cu); -1..-6% at 4000 rows.
+  int pf = osmx_host::tuning().l2_prefetch;
+  if (pf < 0) pf = (g == 32 && V >= 32768 && rows >= 32LL * osmx_host::num_sms() * 2) ? 1 : 0;
   int u8 = osmx_host::tuning().topk_u8;
   // measured (tools/shape_sweep.py, 4000 rows): +8-9% at V = 16K-32K, +1% at
   // 64K, -2% at 128K (rows long enough to amortise the serial load->compute).
@@ -643,6 +647,7 @@ cudaError_t run_rows(const float* x, long long ldx, long long rows, long long V,
     else
       k_topk_rows<32, 128, KC, MODE, 4, 7, 2><<<(unsigned)grid, 128, 0, st>>>(x, ldx, rows, V, k, vals, idx, ws, pf);
   } else if (g == 32 && u8) {
+    pf = osmx_host::tuning().l2_prefetch > 0 ? pf : 0;
     // One wave of rows (<= 28 warps per SM): occupancy is set by the row
     // count, not by registers, so each lane keeps 8 float4s in flight
     // (4-warp CTAs, <= 72 registers: 7 CTAs = 28 warps per SM).

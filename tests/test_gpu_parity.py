@@ -37,7 +37,7 @@ def lib():
     _lib.load()
     yield _lib
     for key, val in (("shape", 0), ("split_chunk", 0), ("tma", 0), ("topk_threads", 0), ("topk_u8", -1),
-                     ("l2_prefetch", 0), ("cluster_size", 0), ("topk_pipe", 0), ("split_cta", 0)):
+                     ("l2_prefetch", -1), ("cluster_size", 0), ("topk_pipe", 0), ("split_cta", 0)):
         _lib.config_set(key, val)
 
 

@@ -1,0 +1,44 @@
+// Read-bandwidth ceiling probe: a persistent grid streams N floats with
+// 128-bit loads (U in flight per thread) and folds them with max -- the
+// access pattern of the fused top-K without its arithmetic.
+#include <cstdio>
+#include <cuda_runtime.h>
+template <int U>
+__global__ void __launch_bounds__(256) rd(const float4* __restrict__ p, size_t n, float* out) {
+  float m = -1e30f;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  for (; i + (U - 1) * stride < n; i += U * stride) {
+    float4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                   : "=f"(v[u].x), "=f"(v[u].y), "=f"(v[u].z), "=f"(v[u].w) : "l"(p + i + u * stride));
+#pragma unroll
+    for (int u = 0; u < U; ++u) m = fmaxf(m, fmaxf(fmaxf(v[u].x, v[u].y), fmaxf(v[u].z, v[u].w)));
+  }
+  for (; i < n; i += stride) m = fmaxf(m, p[i].x);
+  if (m == 12345.0f) *out = m;
+}
+int main() {
+  const size_t bytes = 34359738368ULL;  // the C4 shard
+  float4* p; float* o;
+  cudaMalloc(&p, bytes); cudaMalloc(&o, 4); cudaMemset(p, 0, bytes);
+  int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+  for (int blocks_per_sm : {4, 8}) {
+    for (int u : {4, 8, 16}) {
+      float best = 1e9;
+      for (int r = 0; r < 5; ++r) {
+        cudaEventRecord(a);
+        if (u == 4) rd<4><<<sms * blocks_per_sm, 256>>>(p, bytes / 16, o);
+        if (u == 8) rd<8><<<sms * blocks_per_sm, 256>>>(p, bytes / 16, o);
+        if (u == 16) rd<16><<<sms * blocks_per_sm, 256>>>(p, bytes / 16, o);
+        cudaEventRecord(b); cudaEventSynchronize(b);
+        float ms; cudaEventElapsedTime(&ms, a, b); if (ms < best) best = ms;
+      }
+      printf("blocks/SM %d U %2d: %.3f ms  %.1f GB/s\n", blocks_per_sm, u, best, bytes / (best * 1e-3) / 1e9);
+    }
+  }
+  return 0;
+}
