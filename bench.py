@@ -244,6 +244,9 @@ def main() -> None:
     ap.add_argument("--cpu", default="auto", choices=["auto", "on", "off"])
     ap.add_argument("--sweep-reps", type=int, default=10)
     ap.add_argument("--sweep-only", action="store_true", help="print only the configs[1]/[2]/[4] sweeps (N=1)")
+    ap.add_argument("--vsplit", default="auto", choices=["auto", "on", "off"],
+                    help="configs[4] across ranks: one 2^26 row split over the N GPUs, NCCL record all-gather "
+                         "(auto: when N > 1)")
     args = ap.parse_args()
 
     if args.impl == "reference":
@@ -270,10 +273,16 @@ def main() -> None:
         print(json.dumps({"metric": METRIC, "sweep": sweep}), flush=True)
         return
     dist = None
-    if world > 1:
+    if world > 1 or args.vsplit == "on":
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if not dist.is_initialized():
+            if world == 1:  # a one-rank group, so the V-split's collective runs too
+                os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+                os.environ.setdefault("MASTER_PORT", "29531")
+                dist.init_process_group("nccl", device_id=dev, rank=0, world_size=1)
+            else:
+                dist.init_process_group("nccl", device_id=dev)
 
     from paper_1805_02867_b200 import _lib, osmx
 
@@ -426,10 +435,52 @@ def main() -> None:
     if sweep is not None:
         result["sweep"] = sweep
 
+    # ---- configs[4] across ranks (V-split + NCCL record all-gather)
+    if args.vsplit == "on" or (args.vsplit == "auto" and world > 1):
+        del x
+        torch.cuda.empty_cache()
+        result["vsplit_c5"] = vsplit_measure(dist, dev, world, rank, args.steps, args.warmup)
+
     if rank == 0:
         print(json.dumps(result), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+
+
+def vsplit_measure(dist, dev, world, rank, steps, warmup) -> dict:
+    """configs[4] split across ranks: each rank owns a 64-byte aligned column
+    slice of one 2^26 row, reduces it to one record (warp-per-piece records +
+    in-GPU combine), the N records are all-gathered (one NCCL collective) and
+    every rank merges them in rank order (shard.vsplit_softmax_topk).  Time:
+    CUDA events per rank, max over ranks."""
+    import torch
+
+    from paper_1805_02867_b200 import shard
+
+    V, k = 1 << 26, K_TOP
+    c0, c1 = shard.col_range(V, world, rank)
+    g = torch.Generator(device=dev)
+    g.manual_seed(77)
+    row = torch.empty((1, V), dtype=torch.float32, device=dev).normal_(generator=g)  # same row on every rank
+    xs = row[:, c0:c1].contiguous()
+    del row
+    for _ in range(max(warmup, 1)):
+        vals, idx = shard.vsplit_softmax_topk(xs, c0, k, world)
+    dist.barrier()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(steps):
+        vals, idx = shard.vsplit_softmax_topk(xs, c0, k, world)
+    b.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([a.elapsed_time(b) / steps], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t[0])
+    gbs = algo_bytes("online_fused", 1, V, k) / (ms * 1e-3) / 1e9
+    return {"rows": 1, "V": V, "k": k, "ranks": world, "ms": round(ms, 5), "GBps": round(gbs, 1),
+            "top1_index": int(idx.reshape(-1)[0].item()),
+            "collective": "one all_gather_into_tensor of fixed-size records (NCCL)", "timing": "max over ranks"}
 
 
 def e2e_measure(lib, _lib, x, dev_idx, rows, V, k, dev, world, dist, local) -> dict:
