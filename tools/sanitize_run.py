@@ -1,0 +1,52 @@
+"""Small launches of every kernel family (for compute-sanitizer runs)."""
+import sys
+from pathlib import Path
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import numpy as np
+import torch
+from paper_1805_02867_b200 import _lib, osmx
+
+_lib.load()
+rng = np.random.default_rng(3)
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+cases = [
+    ("resident", {"shape": 1}, [(7, 100), (5, 1023), (3, 2045)]),
+    ("staged", {"shape": 4}, [(300, 3001), (40, 16383)]),
+    ("cluster", {"shape": 5, "cluster_size": 4}, [(40, 70001), (9, 5)]),
+    ("stream", {"shape": 2}, [(3, 40001)]),
+    ("split", {"shape": 3, "split_chunk": 4096}, [(2, 50001)]),
+]
+for name, knobs, shapes in cases:
+    for kk, vv in knobs.items():
+        _lib.config_set(kk, vv)
+    for rows, V in shapes:
+        big = rng.standard_normal((rows, V + 3)).astype(np.float32)
+        xt = dev(big)[:, 1:V + 1]  # misaligned, ld = V + 3
+        for alg in ("naive", "safe", "online"):
+            osmx.softmax(xt, alg=alg)
+        for alg in ("online_fused", "safe_fused", "safe_unfused", "online_unfused"):
+            osmx.softmax_topk(xt, min(5, V), alg=alg)
+        osmx.topk(xt, min(3, V))
+    for kk in knobs:
+        _lib.config_set(kk, 0)
+for knobs in ({"topk_threads": 32, "topk_u8": 1}, {"topk_threads": 32, "topk_pipe": 1}, {"tma": 2},
+              {"topk_threads": 32, "l2_prefetch": 1}):
+    for kk, vv in knobs.items():
+        _lib.config_set(kk, vv)
+    x = dev(rng.standard_normal((64, 20001)).astype(np.float32))
+    osmx.softmax_topk(x, 5)
+    osmx.topk(x, 7)
+    for kk in knobs:
+        _lib.config_set(kk, -1 if kk in ("topk_u8", "l2_prefetch") else 0)
+x = dev(rng.standard_normal((3, 5000)).astype(np.float32))
+osmx.softmax_topk(x, 100)  # large k
+osmx.topk(x, 5000)
+x1 = dev(rng.standard_normal((1, 300000)).astype(np.float32))
+osmx.softmax_topk(x1, 5)  # warp-piece split + combine
+torch.cuda.synchronize()
+print("sanitize run ok")
