@@ -172,6 +172,55 @@ __device__ __forceinline__ void stream_seg_pipe(const Seg& s, int t, F1&& f1, FB
   }
 }
 
+// Same visit order as stream_seg (G threads, U float4s per batch per
+// thread) with the body register-double-buffered: the loads of batch i+1 are
+// issued before batch i is processed, so a warp keeps U float4s in flight
+// while it computes instead of alternating load / compute (the one-wave
+// regime where occupancy, not registers, limits the bytes in flight).
+template <int G, int U, class F1, class FB>
+__device__ __forceinline__ void stream_seg_db(const Seg& s, int t, F1&& f1, FB&& fb) {
+  if (t < s.head) f1(ld_f1(s.p + t), (long long)t);
+  const float* b = s.p + s.head;
+  constexpr long long kB = (long long)U * G;
+  const long long nfull = s.nvec / kB;  // full batches
+  auto load = [&](float4 (&v)[U], long long bi) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = ld_f4(b + 4 * (bi * kB + (long long)u * G + t));
+  };
+  float4 A[U], B[U];
+  long long bi = 0;
+  if (nfull > 0) load(A, 0);
+  while (bi < nfull) {
+    if (bi + 1 < nfull) load(B, bi + 1);
+    fb(A, bi * kB + t, U);
+    if (++bi >= nfull) break;
+    if (bi + 1 < nfull) load(A, bi + 1);
+    fb(B, bi * kB + t, U);
+    ++bi;
+  }
+  // last partial batch
+  const long long q0 = nfull * kB + t;
+  if (nfull * kB < s.nvec) {
+    float4 v[U];
+    int cnt = 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long qq = q0 + (long long)u * G;
+      if (qq < s.nvec) {
+        v[u] = ld_f4(b + 4 * qq);
+        cnt = u + 1;
+      } else {
+        v[u] = make_float4(kNegInf, kNegInf, kNegInf, kNegInf);
+      }
+    }
+    fb(v, q0, cnt);
+  }
+  if (t < s.tail) {
+    const long long j = s.head + 4 * s.nvec + t;
+    f1(ld_f1(s.p + j), j);
+  }
+}
+
 // Same traversal, writing one output per element (y has the same alignment
 // phase as x only when ldx == ldy; the output pointer is aligned
 // independently, falling back to scalar stores when phases differ).

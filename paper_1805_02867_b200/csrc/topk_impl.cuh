@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(BLOCK, MINB)
                 long long chunk = 0, long long col0 = 0, char* __restrict__ rec = nullptr) {
   constexpr int NW = BLOCK / 32;
   constexpr int RPC = BLOCK / G;
-  static_assert(NST == 0 || G == 32, "the cp.async pipeline is per warp");
+  static_assert(NST <= 0 || G == 32, "the cp.async pipeline is per warp");
   __shared__ __align__(16) float4 pipe_buf[NST > 0 ? NW * NST * U * 32 : 1];
   __shared__ float smf[2 * NW];
   __shared__ float sv[NW * KC];
@@ -306,7 +306,11 @@ __global__ void __launch_bounds__(BLOCK, MINB)
       P.R = __frcp_rn(d);
       bad = !(d == d) || !isfinite(M) || !(MN == MN) || MN == kNegInf;
     }
-    if constexpr (NST > 0 && MODE != kModeSafe) {
+    if constexpr (NST < 0 && MODE != kModeSafe) {  // register double buffering
+      stream_seg_db<G, U>(
+          s, t, [&](float v, long long j) { P.scalar(v, (int)j, k); },
+          [&](float4 (&v)[U], long long q0, int cnt) { P.batch(s, v, q0, cnt, k); });
+    } else if constexpr (NST > 0 && MODE != kModeSafe) {
       stream_seg_pipe<U, NST>(
           s, t, [&](float v, long long j) { P.scalar(v, (int)j, k); },
           [&](float4 (&v)[U], long long q0, int cnt) { P.batch(s, v, q0, cnt, k); },
@@ -636,11 +640,21 @@ cudaError_t run_rows(const float* x, long long ldx, long long rows, long long V,
   // measured (tools/shape_sweep.py, 4000 rows): +8-9% at V = 16K-32K, +1% at
   // 64K, -2% at 128K (rows long enough to amortise the serial load->compute).
   if (u8 < 0) u8 = (g == 32 && V >= 8192 && V <= 65536 && rows <= 28LL * osmx_host::num_sms()) ? 1 : 0;
-  const int pipe = V < (1LL << 33) ? osmx_host::tuning().topk_pipe : 0;  // 32-bit float4 counts
+  int pipe = V < (1LL << 33) ? osmx_host::tuning().topk_pipe : 0;  // 32-bit float4 counts
+  // One wave of rows with V >= 16K: register double buffering (2 x 4 float4s
+  // per lane, loads of batch i+1 in flight while batch i is processed):
+  // 4000 rows: +0.4% (32K), +6% (64K), +1.3% (128K) over the U = 8 variant.
+  if (pipe == 0 && osmx_host::tuning().topk_pipe == 0 && g == 32 && V >= 16384 &&
+      rows <= 28LL * osmx_host::num_sms() && osmx_host::tuning().topk_u8 < 0 && osmx_host::tuning().topk_threads == 0)
+    pipe = 4;
   if (g == 32 && pipe > 0) {
     // per-warp cp.async pipeline: 4-warp CTAs, U float4s x NST stages per lane
     const long long grid = std::min<long long>((rows + 3) / 4, 1LL << 30);
-    if (pipe == 1)
+    if (pipe == 4)  // register double buffering, 2 x 4 float4s per lane
+      k_topk_rows<32, 128, KC, MODE, 4, 7, -1><<<(unsigned)grid, 128, 0, st>>>(x, ldx, rows, V, k, vals, idx, ws, pf);
+    else if (pipe == 5)  // register double buffering, 2 x 2 float4s per lane
+      k_topk_rows<32, 128, KC, MODE, 2, 8, -1><<<(unsigned)grid, 128, 0, st>>>(x, ldx, rows, V, k, vals, idx, ws, pf);
+    else if (pipe == 1)
       k_topk_rows<32, 128, KC, MODE, 4, 8, 3><<<(unsigned)grid, 128, 0, st>>>(x, ldx, rows, V, k, vals, idx, ws, pf);
     else if (pipe == 2)
       k_topk_rows<32, 128, KC, MODE, 2, 8, 4><<<(unsigned)grid, 128, 0, st>>>(x, ldx, rows, V, k, vals, idx, ws, pf);
