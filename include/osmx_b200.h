@@ -74,7 +74,8 @@ const char* osmx_last_cuda_error(void);
 /* ---------------------------------------------------------- workspace -- */
 
 /* Bytes of workspace for one call of `alg` on rows x V (k for top-K algs;
- * alg 7 = osmx_topk, 8 = osmx_normalizer, 9 = osmx_slice_record).
+ * alg 7 = osmx_topk, 8 = osmx_normalizer, 9 = osmx_slice_record,
+ * 10 = osmx_proj_softmax_topk with V = vocabulary columns). 
  * Always >= 128 (the status header). */
 size_t osmx_workspace_bytes(int alg, int64_t rows, int64_t V, int32_t k);
 osmx_status osmx_workspace_init(void* ws, size_t ws_bytes, void* stream);
@@ -104,6 +105,16 @@ osmx_status osmx_softmax_topk(int alg, const float* x, int64_t ldx, int64_t rows
 
 /* Top-K of arbitrary values per row.  Replaces topk_of (topk.hpp:54,
  * topk.cpp:20-28). */
+/* The projection layer fused with the online softmax + top-K:
+ * for each of `rows` bf16 vectors h (row-major rows x D) and the bf16 weight
+ * W (row-major V x D), the top-k of softmax(h W^T) -- values e^(z - m)/d and
+ * column indices, ties to the lower column -- without writing the logits z
+ * (tcgen05 tensor cores, fp32 accumulation).  D % 8 == 0, h / W 16-byte
+ * aligned, 1 <= k <= OSMX_MAX_K.  This op has no reference counterpart; its
+ * result equals online_softmax_topk (topk.hpp:68) of the fp32 logits. */
+osmx_status osmx_proj_softmax_topk(const void* h, int64_t rows, int64_t D, const void* w, int64_t V, int32_t k,
+                                   float* vals, int64_t* idx, void* ws, size_t ws_bytes, void* stream);
+
 osmx_status osmx_topk(const float* v, int64_t ld, int64_t rows, int64_t V, int32_t k, float* vals,
                       int64_t* idx, void* ws, size_t ws_bytes, void* stream);
 

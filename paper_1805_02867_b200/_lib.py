@@ -41,6 +41,7 @@ SIGNATURES = {
     "osmx_normalizer": (_int, [_vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _sz, _vp]),
     "osmx_record_bytes": (_sz, [_i32]),
     "osmx_slice_record": (_int, [_vp, _i64, _i64, _i32, _vp, _vp, _sz, _vp]),
+    "osmx_proj_softmax_topk": (_int, [_vp, _i64, _i64, _vp, _i64, _i32, _vp, _vp, _vp, _sz, _vp]),
     "osmx_records_combine": (_int, [_vp, _i32, _i32, _vp, _vp, _vp, _vp, _sz, _vp]),
     "osmx_scale_with_record": (_int, [_vp, _i64, _vp, _vp, _vp]),
     "osmx_softmax_host": (_int, [_int, _vp, _i64, _i64, _vp, _int, _pi64]),

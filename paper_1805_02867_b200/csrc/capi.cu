@@ -65,6 +65,9 @@ static size_t split_region(int alg, long long rows, long long V, int k) {
     case kSliceRecord:  // always the split path (piece records + combine)
       b = topk_split_ws(kOnlineFusedTopk, rows, V, k);
       break;
+    case kProjTopk:
+      b = proj_topk_ws(rows, V, k);
+      break;
     case kSafeUnfusedTopk:
     case kOnlineUnfusedTopk:
     case kTopkOf: {
@@ -221,6 +224,22 @@ osmx_status osmx_topk(const float* v, int64_t ld, int64_t rows, int64_t V, int32
   if (ws_bytes < workspace_bytes(kTopkOf, rows, V, k)) return OSMX_ERR_INVALID_ARG;
   return run_topk_alg(kTopkOf, v, ld, rows, V, k, vals, reinterpret_cast<long long*>(idx), ws, ws_bytes,
                       static_cast<cudaStream_t>(stream));
+}
+
+osmx_status osmx_proj_softmax_topk(const void* h, int64_t rows, int64_t D, const void* w, int64_t V, int32_t k,
+                                   float* vals, int64_t* idx, void* ws, size_t ws_bytes, void* stream) {
+  if (V < 1 || D < 1) return OSMX_ERR_EMPTY;
+  if (k < 1 || (long long)k > V) return OSMX_ERR_INVALID_K;
+  if (k > kMaxK) return OSMX_ERR_UNSUPPORTED;
+  if (rows < 0 || !ws) return OSMX_ERR_INVALID_ARG;
+  if (rows == 0) return OSMX_OK;
+  // TMA: 16-byte aligned bases and row strides (D % 8 bf16), 32-bit coordinates
+  if (!h || !w || !vals || !idx || (D % 8) || ((reinterpret_cast<uintptr_t>(h) | reinterpret_cast<uintptr_t>(w)) & 15) ||
+      rows > (1LL << 31) - 1 || V > (1LL << 31) - 1 || D > (1LL << 31) - 1)
+    return OSMX_ERR_INVALID_ARG;
+  if (ws_bytes < workspace_bytes(kProjTopk, rows, V, k)) return OSMX_ERR_INVALID_ARG;
+  return cuda_status(launch_proj_topk(h, rows, D, w, V, k, vals, reinterpret_cast<long long*>(idx), ws,
+                                      static_cast<cudaStream_t>(stream)));
 }
 
 osmx_status osmx_normalizer(const float* x, int64_t ldx, int64_t rows, int64_t V, int64_t chunk, float* m,

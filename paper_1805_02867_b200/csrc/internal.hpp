@@ -21,6 +21,7 @@ enum Alg : int {
   kTopkOf = 7,
   kNormalizer = 8,
   kSliceRecord = 9,  // osmx_slice_record (workspace sizing only)
+  kProjTopk = 10,    // osmx_proj_softmax_topk (projection fused with the online softmax top-K)
 };
 
 // Kernel-shape families chosen per (rows, V) by the launch layer.
@@ -99,6 +100,12 @@ size_t topk_split_ws(int alg, long long rows, long long V, int k);
 bool topk_split(long long rows, long long V);
 cudaError_t launch_topk_mode(int mode, const float* x, long long ldx, long long rows, long long V,
                              int k, float* vals, long long* idx, void* ws, cudaStream_t st);
+
+// proj_topk.cu: logits = H W^T on tcgen05 tensor cores, never written to
+// HBM; per-(row, 256-column tile) records + the split combine.
+size_t proj_topk_ws(long long rows, long long V, int k);
+cudaError_t launch_proj_topk(const void* h, long long rows, long long D, const void* w, long long V, int k,
+                             float* vals, long long* idx, void* ws, cudaStream_t st);
 
 // Largest k served by the register top-K lists (and by split records).
 constexpr int kMaxK = 32;

@@ -739,8 +739,12 @@ cudaError_t run_split(const float* x, long long ldx, long long rows, long long V
       const long long pieces = rows * R;
       if (pieces <= 28LL * osmx_host::num_sms() && pc >= 8192) {
         const long long grid = (pieces + 3) / 4;
-        k_topk_rows<32, 128, KC, MODE, 8, 7><<<(unsigned)grid, 128, 0, st>>>(x, ldx, pieces, V, k, nullptr, nullptr,
-                                                                          ws, 0, (int)R, pc, col0, rec);
+        if (osmx_host::tuning().topk_pipe == 0)  // one wave: register double buffering
+          k_topk_rows<32, 128, KC, MODE, 4, 7, -1><<<(unsigned)grid, 128, 0, st>>>(x, ldx, pieces, V, k, nullptr,
+                                                                                nullptr, ws, 0, (int)R, pc, col0, rec);
+        else
+          k_topk_rows<32, 128, KC, MODE, 8, 7><<<(unsigned)grid, 128, 0, st>>>(x, ldx, pieces, V, k, nullptr, nullptr,
+                                                                            ws, 0, (int)R, pc, col0, rec);
       } else {
         const long long grid = std::min<long long>((pieces + 7) / 8, 1LL << 30);
         k_topk_rows<32, 256, KC, MODE, 4, 4><<<(unsigned)grid, 256, 0, st>>>(x, ldx, pieces, V, k, nullptr, nullptr,

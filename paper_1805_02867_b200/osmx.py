@@ -357,6 +357,33 @@ def softmax_topk(x, k: int, alg: str = "online_fused", check: bool = True, out=N
     return vals, idx
 
 
+def proj_softmax_topk(h, w, k: int, check: bool = True):
+    """Top-k of softmax(h @ w.T) per row without materialising the logits
+    (osmx_proj_softmax_topk: tcgen05 GEMM tiles reduced to (m, d, top-k)
+    records in the epilogue).  h: rows x D, w: V x D, both CUDA bfloat16,
+    row-major, D % 8 == 0.  Returns (values rows x k, int64 indices)."""
+    import torch
+
+    if h.dtype != torch.bfloat16 or w.dtype != torch.bfloat16 or not (h.is_cuda and w.is_cuda):
+        raise TypeError("proj_softmax_topk takes CUDA bfloat16 h and w")
+    if h.dim() != 2 or w.dim() != 2 or h.shape[1] != w.shape[1]:
+        raise ValueError("h must be rows x D and w V x D")
+    h = h.contiguous()
+    w = w.contiguous()
+    rows, D = h.shape
+    V = w.shape[0]
+    vals = torch.empty((rows, max(k, 1)), dtype=torch.float32, device=h.device)
+    idx = torch.empty((rows, max(k, 1)), dtype=torch.int64, device=h.device)
+    stream = _stream_ptr(h.device)
+    ws, nb = workspace(10, rows, V, k, h.device)
+    st = load().osmx_proj_softmax_topk(h.data_ptr(), rows, D, w.data_ptr(), V, k, vals.data_ptr(), idx.data_ptr(),
+                                       ws.data_ptr(), ws.numel(), stream)
+    _raise(st)
+    if check:
+        check_status(ws, stream)
+    return vals, idx
+
+
 def topk(v, k: int, check: bool = True):
     """Batched topk_of over a CUDA float32 tensor of values."""
     import torch
