@@ -98,36 +98,45 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
 }
-
+// Persistent: one CTA per SM walks the (row tile, vocabulary tile) grid,
+// row tiles fastest (the CTAs in flight cover every row tile of a few
+// vocabulary tiles, so each W tile is read from HBM once and shared through
+// L2; H stays L2-resident).  Two 256-column TMEM accumulators: the MMA warp
+// fills one while the epilogue warps drain the other, and the TMA producer
+// runs ahead across tile boundaries -- the epilogue and the pipeline fill
+// are hidden behind the tensor-core mainloop.
 template <int KC>
 __global__ void __launch_bounds__(kProjThreads, 1)
     k_proj_topk(const __grid_constant__ CUtensorMap tmap_h, const __grid_constant__ CUtensorMap tmap_w, int rows,
-                int D, int V, int k, char* __restrict__ rec) {
+                int D, int V, int k, char* __restrict__ rec, int MT, int NT) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  // 1024-byte alignment of every stage (swizzle atoms)
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
   uint64_t* empty = full + kStages;
-  uint64_t* accum = empty + kStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+  uint64_t* afull = empty + kStages;  // [2] accumulator ready (MMA commit)
+  uint64_t* aempty = afull + 2;       // [2] accumulator drained (4 epilogue warps)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n0 = blockIdx.x * kBN, m0 = blockIdx.y * kBM;
   const int nk = (D + kBK - 1) / kBK;
+  const int ntiles = MT * NT;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(accum, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&afull[b], 1);
+      mbar_init(&aempty[b], 4);
+    }
     fence_mbar_init();
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_h) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_w) : "memory");
   }
-  if (warp == 2) {  // TMEM: 256 fp32 columns x 128 lanes for the accumulator
+  if (warp == 2) {  // TMEM: 2 x 256 fp32 columns x 128 lanes
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(kBN)
+                 "r"(2 * kBN)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -138,108 +147,133 @@ __global__ void __launch_bounds__(kProjThreads, 1)
 
   if (warp == 0 && lane == 0) {
     // ------------------------------------------------------------ producer
-    for (int kc = 0; kc < nk; ++kc) {
-      const int s = kc % kStages;
-      if (kc >= kStages) mbar_wait_b(&empty[s], (uint32_t)(((kc / kStages) - 1) & 1));
-      unsigned char* a = smem + s * kStageBytes;
-      mbar_arrive_expect_tx(&full[s], (uint32_t)kStageBytes);
-      tma_load_2d(a, &tmap_h, kc * kBK, m0, &full[s]);
-      tma_load_2d(a + kABytes, &tmap_w, kc * kBK, n0, &full[s]);
+    long long g = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const int m0 = (t % MT) * kBM, n0 = (t / MT) * kBN;
+      for (int kc = 0; kc < nk; ++kc, ++g) {
+        const int s = (int)(g % kStages);
+        if (g >= kStages) mbar_wait_b(&empty[s], (uint32_t)(((g / kStages) - 1) & 1));
+        unsigned char* a = smem + s * kStageBytes;
+        mbar_arrive_expect_tx(&full[s], (uint32_t)kStageBytes);
+        tma_load_2d(a, &tmap_h, kc * kBK, m0, &full[s]);
+        tma_load_2d(a + kABytes, &tmap_w, kc * kBK, n0, &full[s]);
+      }
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------------------------------------------------- MMA issuer
-    for (int kc = 0; kc < nk; ++kc) {
-      const int s = kc % kStages;
-      mbar_wait_b(&full[s], (uint32_t)((kc / kStages) & 1));
+    long long g = 0;
+    int i = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+      const int b = i & 1;
+      if (i >= 2) mbar_wait_b(&aempty[b], (uint32_t)(((i >> 1) - 1) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t a = smem_u32(smem + s * kStageBytes);
-      const uint64_t ad = umma_desc_sw128(a), bd = umma_desc_sw128(a + kABytes);
+      const uint32_t acc_t = tmem + (uint32_t)(b * kBN);
+      for (int kc = 0; kc < nk; ++kc, ++g) {
+        const int s = (int)(g % kStages);
+        mbar_wait_b(&full[s], (uint32_t)((g / kStages) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t a = smem_u32(smem + s * kStageBytes);
+        const uint64_t ad = umma_desc_sw128(a), bd = umma_desc_sw128(a + kABytes);
 #pragma unroll
-      for (int kk = 0; kk < kBK / 16; ++kk)  // K 16 per MMA = 32 bytes along the swizzled row
-        umma_bf16(tmem, ad + (uint64_t)((kk * 32) >> 4), bd + (uint64_t)((kk * 32) >> 4), (kc | kk) != 0);
-      umma_commit(&empty[s]);  // stage free once these MMAs have read it
+        for (int kk = 0; kk < kBK / 16; ++kk)  // K 16 per MMA = 32 bytes along the swizzled row
+          umma_bf16(acc_t, ad + (uint64_t)((kk * 32) >> 4), bd + (uint64_t)((kk * 32) >> 4), (kc | kk) != 0);
+        umma_commit(&empty[s]);  // stage free once these MMAs have read it
+      }
+      umma_commit(&afull[b]);  // accumulator b complete
     }
-    umma_commit(accum);
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
-    mbar_wait_b(accum, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const int q = warp & 3;             // TMEM lane quadrant of this warp
-    const int r = q * 32 + lane;        // tile row = TMEM lane
-    const int row = m0 + r;
-    L2Acc acc;
-    TopList<KC> L;
-    L.init(k);
-    float mn = -kNegInf;
+    const int q = warp & 3;       // TMEM lane quadrant of this warp
+    const int r = q * 32 + lane;  // tile row = TMEM lane
+    int i = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+      const int b = i & 1;
+      const int m0 = (t % MT) * kBM, nt = t / MT, n0 = nt * kBN;
+      const int row = m0 + r;
+      mbar_wait_b(&afull[b], (uint32_t)((i >> 1) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      L2Acc acc;
+      TopList<KC> L;
+      L.init(k);
+      float mn = -kNegInf;
 #pragma unroll 1
-    for (int c = 0; c < kBN; c += 32) {
-      uint32_t u[32];
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
-          "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-          : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]), "=r"(u[7]),
-            "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]), "=r"(u[12]), "=r"(u[13]), "=r"(u[14]), "=r"(u[15]),
-            "=r"(u[16]), "=r"(u[17]), "=r"(u[18]), "=r"(u[19]), "=r"(u[20]), "=r"(u[21]), "=r"(u[22]), "=r"(u[23]),
-            "=r"(u[24]), "=r"(u[25]), "=r"(u[26]), "=r"(u[27]), "=r"(u[28]), "=r"(u[29]), "=r"(u[30]), "=r"(u[31])
-          : "r"(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      float4 v[8];
+      for (int c = 0; c < kBN; c += 32) {
+        uint32_t u[32];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"
+            "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]), "=r"(u[7]),
+              "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]), "=r"(u[12]), "=r"(u[13]), "=r"(u[14]),
+              "=r"(u[15]), "=r"(u[16]), "=r"(u[17]), "=r"(u[18]), "=r"(u[19]), "=r"(u[20]), "=r"(u[21]),
+              "=r"(u[22]), "=r"(u[23]), "=r"(u[24]), "=r"(u[25]), "=r"(u[26]), "=r"(u[27]), "=r"(u[28]),
+              "=r"(u[29]), "=r"(u[30]), "=r"(u[31])
+            : "r"(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * kBN + c)));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        float4 v[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        float z[4];
+        for (int j = 0; j < 8; ++j)
+          v[j] = make_float4(__uint_as_float(u[4 * j]), __uint_as_float(u[4 * j + 1]), __uint_as_float(u[4 * j + 2]),
+                             __uint_as_float(u[4 * j + 3]));
+        if (n0 + c + 32 > V) {  // the vocabulary ends inside this chunk: mask (TMA zero fill)
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int col = n0 + c + 4 * i + e;
-          z[e] = (col < V) ? __uint_as_float(u[4 * i + e]) : kNegInf;
+          for (int j = 0; j < 8; ++j) {
+            const int col = n0 + c + 4 * j;
+            if (col + 0 >= V) v[j].x = kNegInf;
+            if (col + 1 >= V) v[j].y = kNegInf;
+            if (col + 2 >= V) v[j].z = kNegInf;
+            if (col + 3 >= V) v[j].w = kNegInf;
+          }
         }
-        v[i] = make_float4(z[0], z[1], z[2], z[3]);
-      }
-      float bm = kNegInf;
+        float bm = kNegInf, bn = -kNegInf;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        bm = fmaxf(bm, fmaxf(fmaxf(v[i].x, v[i].y), fmaxf(v[i].z, v[i].w)));
-        const int col = n0 + c + 4 * i;
-        if (col < V) mn = fminf(mn, v[i].x);
-        if (col + 1 < V) mn = fminf(mn, v[i].y);
-        if (col + 2 < V) mn = fminf(mn, v[i].z);
-        if (col + 3 < V) mn = fminf(mn, v[i].w);
-      }
-      if (bm != kNegInf) {
-        acc.raise(bm);
-        acc.add_batch<8>(v);
-      }
-      // columns in increasing order: the strict '>' insertion keeps ties on the lower column
-      if (bm > L.thr()) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int col = c + 4 * i;
-          L.offer(v[i].x, col);
-          L.offer(v[i].y, col + 1);
-          L.offer(v[i].z, col + 2);
-          L.offer(v[i].w, col + 3);
+        for (int j = 0; j < 8; ++j) {
+          bm = fmaxf(bm, fmaxf(fmaxf(v[j].x, v[j].y), fmaxf(v[j].z, v[j].w)));
+          // masked lanes are -inf; min over real columns only matters for
+          // the non-finite check, and real logits are finite or NaN
+          if (n0 + c + 4 * j + 3 < V) bn = fminf(bn, fminf(fminf(v[j].x, v[j].y), fminf(v[j].z, v[j].w)));
         }
+        mn = fminf(mn, bn);
+        if (bm != kNegInf) {
+          acc.raise(bm);
+          acc.add_batch<8>(v);
+        }
+        // columns in increasing order: strict '>' keeps ties on the lower column
+        if (bm > L.thr()) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            if (!(fmaxf(fmaxf(v[j].x, v[j].y), fmaxf(v[j].z, v[j].w)) > L.thr())) continue;
+            const int col = c + 4 * j;
+            L.offer(v[j].x, col);
+            L.offer(v[j].y, col + 1);
+            L.offer(v[j].z, col + 2);
+            L.offer(v[j].w, col + 3);
+          }
+        }
+      }
+      // accumulator b is in registers now: hand it back to the MMA warp
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&aempty[b]);
+      if (row < rows) {
+        const MD md = acc.finish();
+        char* my = rec + ((size_t)row * NT + nt) * rec_bytes_(k);
+        *reinterpret_cast<RecHdr*>(my) = RecHdr{md.m, md.d, mn, k};
+        float* rv = reinterpret_cast<float*>(my + rec_vals_off());
+        long long* ri = reinterpret_cast<long long*>(my + rec_idx_off(k));
+        L.normalize(k);
+#pragma unroll
+        for (int s2 = 0; s2 < KC; ++s2)
+          if (s2 < k) {
+            rv[s2] = L.v[s2];
+            ri[s2] = L.i[s2] < 0 ? -1LL : (long long)(n0 + L.i[s2]);
+          }
       }
     }
-    if (row < rows) {
-      const MD md = acc.finish();
-      char* my = rec + ((size_t)row * gridDim.x + blockIdx.x) * rec_bytes_(k);
-      *reinterpret_cast<RecHdr*>(my) = RecHdr{md.m, md.d, mn, k};
-      float* rv = reinterpret_cast<float*>(my + rec_vals_off());
-      long long* ri = reinterpret_cast<long long*>(my + rec_idx_off(k));
-      L.normalize(k);
-#pragma unroll
-      for (int s = 0; s < KC; ++s)
-        if (s < k) {
-          rv[s] = L.v[s];
-          ri[s] = L.i[s] < 0 ? -1LL : (long long)(n0 + L.i[s]);
-        }
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   }
   __syncthreads();
   if (warp == 2) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kBN) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * kBN) : "memory");
   }
 }
 
@@ -277,16 +311,18 @@ cudaError_t run_proj(const void* h, long long rows, long long D, const void* w, 
                      long long* idx, void* ws, cudaStream_t st) {
   CUtensorMap mh, mw;
   if (!make_map(&mh, h, D, rows, kBM) || !make_map(&mw, w, D, V, kBN)) return cudaErrorInvalidValue;
+  auto kern = k_proj_topk<KC>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_proj_topk<KC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kProjSmem);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kProjSmem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  const int nt = (int)((V + kBN - 1) / kBN);
+  const int MT = (int)((rows + kBM - 1) / kBM), nt = (int)((V + kBN - 1) / kBN);
   char* rec = static_cast<char*>(ws) + kWsHeader;
-  dim3 grid((unsigned)nt, (unsigned)((rows + kBM - 1) / kBM));
-  k_proj_topk<KC><<<grid, kProjThreads, kProjSmem, st>>>(mh, mw, (int)rows, (int)D, (int)V, k, rec);
+  const long long tiles = (long long)MT * nt;
+  const int grid = (int)std::min<long long>(tiles, osmx_host::num_sms());
+  kern<<<grid, kProjThreads, kProjSmem, st>>>(mh, mw, (int)rows, (int)D, (int)V, k, rec, MT, nt);
   osmx_host::count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;

@@ -13,7 +13,8 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("rows,D,V,k", [(128, 64, 256, 5), (200, 256, 3000, 5), (129, 520, 4097, 8),
-                                        (512, 1024, 32768, 5), (64, 4096, 20000, 32), (300, 128, 700, 1)])
+                                        (512, 1024, 32768, 5), (64, 4096, 20000, 32), (300, 128, 700, 1),
+                                        (1000, 512, 70000, 5)])
 def test_proj_topk_vs_reference_on_fp32_logits(cuda, oracle_mod, rows, D, V, k):
     import torch
 
