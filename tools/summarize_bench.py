@@ -27,3 +27,5 @@ if sw:
               f"{r.get('online_unfused_stream', {}).get('ms', 0):>9} {r.get('fused_over_online_unfused_stream', 0):>6}")
     if "c5" in sw:
         print("c5", json.dumps(sw["c5"]))
+    if "proj_fused" in sw:
+        print("proj", json.dumps(sw["proj_fused"]))
