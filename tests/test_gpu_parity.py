@@ -388,13 +388,17 @@ def test_large_k(cuda, oracle_mod, lib, k):
         for d in ("normal", "quantized2", "equal", "descending", "spikes"):
             x = dist(d, rng, 4, V)
             vals, idx = osmx.softmax_topk(_dev(x), kk, alg="online_fused")
-            rv, rz = _topk_ref(oracle_mod, "online_softmax_topk", x, kk)
-            assert np.array_equal(idx.cpu().numpy(), rz), (V, kk, d)
-            assert max_rel(vals.cpu().numpy(), rv) <= TOL
+            fv, fz = _topk_ref(oracle_mod, "online_softmax_topk", x, kk)
+            assert np.array_equal(idx.cpu().numpy(), fz), (V, kk, d)
+            assert max_rel(vals.cpu().numpy(), fv) <= TOL
             tv, ti = osmx.topk(_dev(x), kk)
             rv, rz = _topk_ref(oracle_mod, "topk_of", x, kk)
             assert np.array_equal(ti.cpu().numpy(), rz), (V, kk, d)
             assert np.array_equal(tv.cpu().numpy().view(np.int32), rv.view(np.int32))
+            if V == 4099 and d == "normal":  # the reference-shaped host API (numpy in/out), same device path
+                r = osmx.online_softmax_topk(x, kk)
+                assert np.array_equal(np.asarray(r.indices), fz)
+                assert max_rel(np.asarray(r.values), fv) <= TOL
             for alg, op in (("safe_fused", "safe_softmax_fused_topk"), ("safe_unfused", "safe_softmax_then_topk")):
                 vals, idx = osmx.softmax_topk(_dev(x), kk, alg=alg)
                 y, _ = oracle_mod.batch("safe_softmax", x)

@@ -2,6 +2,7 @@
 // 128-bit loads (U in flight per thread) and folds them with max -- the
 // access pattern of the fused top-K without its arithmetic.
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 template <int U>
 __global__ void __launch_bounds__(256) rd(const float4* __restrict__ p, size_t n, float* out) {
@@ -20,8 +21,8 @@ __global__ void __launch_bounds__(256) rd(const float4* __restrict__ p, size_t n
   for (; i < n; i += stride) m = fmaxf(m, p[i].x);
   if (m == 12345.0f) *out = m;
 }
-int main() {
-  const size_t bytes = 34359738368ULL;  // the C4 shard
+int main(int argc, char** argv) {
+  const size_t bytes = argc > 1 ? (size_t)atoll(argv[1]) : 34359738368ULL;  // default: the C4 shard
   float4* p; float* o;
   cudaMalloc(&p, bytes); cudaMalloc(&o, 4); cudaMemset(p, 0, bytes);
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -29,7 +30,7 @@ int main() {
   for (int blocks_per_sm : {4, 8}) {
     for (int u : {4, 8, 16}) {
       float best = 1e9;
-      for (int r = 0; r < 5; ++r) {
+      for (int r = 0; r < 20; ++r) {
         cudaEventRecord(a);
         if (u == 4) rd<4><<<sms * blocks_per_sm, 256>>>(p, bytes / 16, o);
         if (u == 8) rd<8><<<sms * blocks_per_sm, 256>>>(p, bytes / 16, o);
