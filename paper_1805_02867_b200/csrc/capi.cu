@@ -328,7 +328,7 @@ osmx_status osmx_config_set(const char* key, int64_t value) {
     if (value < 0 || value > 1) return OSMX_ERR_INVALID_ARG;
     t.split_cta = (int)value;
   } else if (!strcmp(key, "topk_pipe")) {
-    if (value < 0 || value > 5) return OSMX_ERR_INVALID_ARG;
+    if (value < 0 || value > 6) return OSMX_ERR_INVALID_ARG;
     t.topk_pipe = (int)value;
   } else if (!strcmp(key, "topk_u8")) {
     if (value < -1 || value > 1) return OSMX_ERR_INVALID_ARG;

@@ -221,6 +221,86 @@ __device__ __forceinline__ void stream_seg_db(const Seg& s, int t, F1&& f1, FB&&
   }
 }
 
+// Same visit order as stream_seg for one warp (G = 32), the body streamed
+// through a per-warp ring of NS shared-memory stages of U*32 float4s by 1-D
+// bulk copies (cp.async.bulk, one instruction per 2 KB chunk, issued by lane
+// 0, completing on the stage's mbarrier): NS chunks stay in flight without
+// registers, and a chunk is refilled as soon as the warp has it in
+// registers.  `g` is the warp's running chunk count (stage / parity across
+// rows); ring = NS*U*32 float4s, bars = NS mbarriers, both private to the warp.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+      "l"(src), "r"(bytes), "r"(static_cast<unsigned>(__cvta_generic_to_shared(bar)))
+      : "memory");
+}
+__device__ __forceinline__ void bar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   static_cast<unsigned>(__cvta_generic_to_shared(bar))),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* bar, unsigned parity) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  unsigned done;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+template <int U, int NS, class F1, class FB>
+__device__ __forceinline__ void stream_seg_bulk(const Seg& s, int t, F1&& f1, FB&& fb, float4* ring, uint64_t* bars,
+                                                long long& g) {
+  if (t < s.head) f1(ld_f1(s.p + t), (long long)t);
+  constexpr int kB = U * 32;  // float4s per chunk
+  const long long nvec = s.nvec;
+  const long long nch = (nvec + kB - 1) / kB;
+  const float4* body = reinterpret_cast<const float4*>(s.p + s.head);
+  const long long g0 = g;
+  auto issue = [&](long long c) {  // lane 0: chunk c of this row into stage (g0 + c) % NS
+    const int st = (int)((g0 + c) % NS);
+    const long long q0 = c * kB;
+    const unsigned bytes = (unsigned)(16 * (nvec - q0 < kB ? nvec - q0 : kB));
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior reads of the stage before the async write
+    bar_expect_tx(&bars[st], bytes);
+    bulk_g2s(ring + st * kB, body + q0, bytes, &bars[st]);
+  };
+  if (t == 0)
+    for (long long c = 0; c < nch && c < NS; ++c) issue(c);
+  for (long long c = 0; c < nch; ++c) {
+    const int st = (int)((g0 + c) % NS);
+    bar_wait(&bars[st], (unsigned)(((g0 + c) / NS) & 1));
+    const float4* sb = ring + st * kB;
+    const long long q0 = c * kB + t;
+    float4 v[U];
+    int cnt = 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (q0 + u * 32 < nvec) {
+        v[u] = sb[u * 32 + t];
+        cnt = u + 1;
+      } else {
+        v[u] = make_float4(kNegInf, kNegInf, kNegInf, kNegInf);
+      }
+    }
+    __syncwarp();
+    if (t == 0 && c + NS < nch) issue(c + NS);
+    fb(v, q0, cnt);
+  }
+  g = g0 + nch;
+  if (t < s.tail) {
+    const long long j = s.head + 4 * s.nvec + t;
+    f1(ld_f1(s.p + j), j);
+  }
+}
+
 // Same traversal, writing one output per element (y has the same alignment
 // phase as x only when ldx == ldy; the output pointer is aligned
 // independently, falling back to scalar stores when phases differ).

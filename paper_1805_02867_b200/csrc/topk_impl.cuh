@@ -255,7 +255,8 @@ __global__ void __launch_bounds__(BLOCK, MINB)
   constexpr int NW = BLOCK / 32;
   constexpr int RPC = BLOCK / G;
   static_assert(NST <= 0 || G == 32, "the cp.async pipeline is per warp");
-  __shared__ __align__(16) float4 pipe_buf[NST > 0 ? NW * NST * U * 32 : 1];
+  __shared__ __align__(16) float4 pipe_buf[NST > 0 ? NW * NST * U * 32 : (NST == -2 ? NW * 3 * U * 32 : 1)];
+  __shared__ __align__(8) uint64_t bulk_bar[NST == -2 ? NW * 3 : 1];  // per-warp bulk ring (NST = -2)
   __shared__ float smf[2 * NW];
   __shared__ float sv[NW * KC];
   __shared__ int si[NW * KC];
@@ -263,7 +264,17 @@ __global__ void __launch_bounds__(BLOCK, MINB)
   const int t = threadIdx.x % G;
   const long long nrow_groups = (rows + RPC - 1) / RPC;
   if (threadIdx.x == 0) tsh[0] = tsh[1] = Pass<KC, U, MODE, G>::f2o(kNegInf);
+  if constexpr (NST == -2) {
+    if (threadIdx.x == 0) {
+      for (int b = 0; b < NW * 3; ++b)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
+                         static_cast<unsigned>(__cvta_generic_to_shared(&bulk_bar[b])))
+                     : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+  }
   __syncthreads();
+  long long bulk_g = 0;  // per-warp running chunk count of the bulk ring
   int it = 0;
   for (long long rg = blockIdx.x; rg < nrow_groups; rg += gridDim.x, ++it) {
     // slot it&1 serves this row; the other slot is reset for the next row
@@ -306,7 +317,13 @@ __global__ void __launch_bounds__(BLOCK, MINB)
       P.R = __frcp_rn(d);
       bad = !(d == d) || !isfinite(M) || !(MN == MN) || MN == kNegInf;
     }
-    if constexpr (NST < 0 && MODE != kModeSafe) {  // register double buffering
+    if constexpr (NST == -2 && MODE != kModeSafe) {  // per-warp bulk-copy ring, 3 stages
+      const int wv = threadIdx.x >> 5;
+      stream_seg_bulk<U, 3>(
+          s, t, [&](float v, long long j) { P.scalar(v, (int)j, k); },
+          [&](float4 (&v)[U], long long q0, int cnt) { P.batch(s, v, q0, cnt, k); }, pipe_buf + wv * 3 * U * 32,
+          bulk_bar + wv * 3, bulk_g);
+    } else if constexpr (NST == -1 && MODE != kModeSafe) {  // register double buffering
       stream_seg_db<G, U>(
           s, t, [&](float v, long long j) { P.scalar(v, (int)j, k); },
           [&](float4 (&v)[U], long long q0, int cnt) { P.batch(s, v, q0, cnt, k); });
@@ -650,7 +667,9 @@ cudaError_t run_rows(const float* x, long long ldx, long long rows, long long V,
   if (g == 32 && pipe > 0) {
     // per-warp cp.async pipeline: 4-warp CTAs, U float4s x NST stages per lane
     const long long grid = std::min<long long>((rows + 3) / 4, 1LL << 30);
-    if (pipe == 4)  // register double buffering, 2 x 4 float4s per lane
+    if (pipe == 6)  // per-warp bulk-copy ring: 3 x 2 KB chunks in flight per warp
+      k_topk_rows<32, 128, KC, MODE, 4, 7, -2><<<(unsigned)grid, 128, 0, st>>>(x, ldx, rows, V, k, vals, idx, ws, pf);
+    else if (pipe == 4)  // register double buffering, 2 x 4 float4s per lane
       k_topk_rows<32, 128, KC, MODE, 4, 7, -1><<<(unsigned)grid, 128, 0, st>>>(x, ldx, rows, V, k, vals, idx, ws, pf);
     else if (pipe == 5)  // register double buffering, 2 x 2 float4s per lane
       k_topk_rows<32, 128, KC, MODE, 2, 8, -1><<<(unsigned)grid, 128, 0, st>>>(x, ldx, rows, V, k, vals, idx, ws, pf);

@@ -26,6 +26,7 @@ TOPK_VARIANTS = {
     "warp_pipe1": [("topk_threads", 32), ("topk_pipe", 1)], "warp_pipe2": [("topk_threads", 32), ("topk_pipe", 2)],
     "warp_pipe3": [("topk_threads", 32), ("topk_pipe", 3)],
     "warp_db4": [("topk_threads", 32), ("topk_pipe", 4)], "warp_db2": [("topk_threads", 32), ("topk_pipe", 5)],
+    "warp_bulk": [("topk_threads", 32), ("topk_pipe", 6)],
     "split_cta": [("shape", 3), ("split_chunk", 2048), ("split_cta", 1)],
     "split_auto": [("shape", 3)],
 }
@@ -337,7 +338,7 @@ def test_softmax_staged_ring_wrap(cuda, oracle_mod, lib, alg):
 
 
 @pytest.mark.parametrize("variant", ["auto", "warp", "warp_u8", "warp_pf", "warp_pipe1", "warp_pipe3", "warp_db4",
-                                     "warp_db2"])
+                                     "warp_db2", "warp_bulk"])
 def test_online_fused_topk_many_rows(cuda, oracle_mod, lib, variant):
     """Row counts around one wave of warps (the u8 heuristic's range)."""
     from paper_1805_02867_b200 import osmx
