@@ -242,7 +242,7 @@ def main() -> None:
     ap.add_argument("--sweep", default="auto", choices=["auto", "on", "off"])
     ap.add_argument("--e2e", default="auto", choices=["auto", "on", "off"])
     ap.add_argument("--cpu", default="auto", choices=["auto", "on", "off"])
-    ap.add_argument("--sweep-reps", type=int, default=10)
+    ap.add_argument("--sweep-reps", type=int, default=20)
     ap.add_argument("--sweep-only", action="store_true", help="print only the configs[1]/[2]/[4] sweeps (N=1)")
     ap.add_argument("--vsplit", default="auto", choices=["auto", "on", "off"],
                     help="configs[4] across ranks: one 2^26 row split over the N GPUs, NCCL record all-gather "
@@ -433,6 +433,7 @@ def main() -> None:
         ss.start()
         sweep = run_sweeps(lib, _lib, dev, sp, args.sweep_reps, measured_peaks()["hbm_gbs"])
         sweep["clocks"] = ss.stop()
+        sweep["c1_parity"] = c1_parity(lib, _lib, dev)
         result["sweep"] = sweep
         torch.cuda.empty_cache()
 
@@ -543,9 +544,48 @@ def cpu_baseline(x, V, k) -> dict:
     xs = x[:n].cpu().numpy()
     t, kind, _ = reference_rate(xs, V, k, threads)
     gbs = algo_bytes("online_fused", n, V, k) / t / 1e9
+    # single-thread rate on a smaller sample (threads = 1 and all)
+    n1 = max(8, n // max(threads, 1))
+    t1, _, _ = reference_rate(x[:n1].cpu().numpy(), V, k, 1)
     return {"value": round(gbs, 4), "unit": "GB/s", "cores": threads, "kind": kind,
             "sample": f"{n} of the C4 rows (V={V}), reference online_softmax_topk, {threads} threads",
-            "seconds": round(t, 3), "rows_per_s": round(n / t, 2), "elements_per_s": round(n * V / t, 1)}
+            "seconds": round(t, 3), "rows_per_s": round(n / t, 2), "elements_per_s": round(n * V / t, 1),
+            "single_thread_GBps": round(algo_bytes("online_fused", n1, V, k) / t1 / 1e9, 4),
+            "cpu_model": cpu_model()}
+
+
+def cpu_model() -> str:
+    """/proc/cpuinfo model name (osmx_bench.cpp:24-34)."""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def c1_parity(lib, _lib, dev) -> dict:
+    """configs[0] (C1): online softmax over 4000 x 1000 checked against the
+    reference's naive / safe / online softmax on the same rows (the reference
+    library itself, oracle/_ref, on the host), max relative error per alg."""
+    import numpy as np
+    import torch
+
+    from oracle import oracle as O
+    from paper_1805_02867_b200 import osmx
+
+    have_ref = O.ref_available()
+    xs = O.generate_inputs(1, 4000, 1000) if have_ref else host_rows(1, 4000, 1000)
+    xd = torch.from_numpy(np.ascontiguousarray(xs)).to(dev)
+    out = {"rows": 4000, "V": 1000, "checker": "reference library (oracle/_ref)" if have_ref else "oracle port",
+           "inputs": "reference generate_inputs(seed 1)" if have_ref else "numpy normal (seed 1)"}
+    for name in ("naive", "safe", "online"):
+        y = osmx.softmax(xd, alg=name).cpu().numpy().astype(np.float64)
+        ref, st = O.batch(f"{name}_softmax", xs, impl="ref" if have_ref else "port")
+        m = ref > 1e-30
+        out[f"{name}_max_rel_err"] = float(np.max(np.abs(y[m] - ref[m]) / ref[m]))
+    return out
 
 
 def time_rotating(launch, n_sets: int, reps: int, graph: bool = True):

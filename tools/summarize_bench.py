@@ -27,5 +27,7 @@ if sw:
               f"{r.get('online_unfused_stream', {}).get('ms', 0):>9} {r.get('fused_over_online_unfused_stream', 0):>6}")
     if "c5" in sw:
         print("c5", json.dumps(sw["c5"]))
+    if "c1_parity" in sw:
+        print("c1", json.dumps(sw["c1_parity"]))
     if "proj_fused" in sw:
         print("proj", json.dumps(sw["proj_fused"]))
