@@ -702,15 +702,16 @@ cudaError_t launch_alg(const float* x, long long ldx, float* y, long long ldy, l
   int shape = tn.shape;
   if (shape == osmx_host::kShapeAuto) {
     // Measured on B200 (tools/shape_sweep.py, inputs out of L2, 4000 and
-    // 32768 rows): register-resident rows win up to V ~ 1024; the TMA-staged
+    // 32768 rows): register-resident rows win up to V ~ 2048; the TMA-staged
     // shared-memory ring from there to 16K (1.1-1.5x the resident / stream
-    // kernels at V = 3K-10K); beyond, the stream kernel (one CTA per row) or
-    // the split kernel when there are too few rows to fill the SMs.
+    // kernels at V = 3K-10K), cluster-staged rows up to 16 x 12288; beyond,
+    // the stream kernel (one CTA per row) or the split kernel when there are
+    // too few rows to fill the SMs.
     if (V <= osmx_host::resident_limit(vec))
       shape = osmx_host::kShapeResident;
     else if (V <= kStagedMaxV)
       shape = osmx_host::kShapeStaged;
-    else if (V <= kClusterMaxV && rows >= osmx_host::num_sms() / 2)
+    else if (V <= cluster_max_v<ALG>() && rows >= osmx_host::num_sms() / 2)
       shape = osmx_host::kShapeCluster;
     else if (rows >= 2LL * osmx_host::num_sms())
       shape = osmx_host::kShapeStream;

@@ -457,7 +457,15 @@ __global__ void __launch_bounds__(1024, 1)
 constexpr int kStagedSmemMax = 227 * 1024;
 constexpr long long kStagedMaxV = 16384;   // one CTA per row up to here
 constexpr long long kClusterSlice = 12288;  // target slice per CTA above
-constexpr long long kClusterMaxV = 10 * kClusterSlice;  // clusters of > 10 CTAs pack badly into GPCs (measured)
+// Clusters of 11..15 CTAs pack badly into GPCs, 16 (non-portable) packs
+// well enough to beat the 4-access stream kernel for safe softmax (4000 x
+// 177828: 1.13 vs 1.70 ms) but not reliably the 3-access online / naive
+// ones (150001: 1.18 vs 1.10 ms online) -- so those stop at 10 CTAs.
+constexpr long long kClusterMaxV = 16 * kClusterSlice;
+template <int ALG>
+constexpr long long cluster_max_v() {
+  return ALG == osmx_host::kSafe ? 16 * kClusterSlice : 10 * kClusterSlice;
+}
 
 // Launch one (GW, NG, C) layout.  NG is clamped so that D >= NG + 1.
 template <int GW, int ALG>
@@ -520,7 +528,7 @@ inline int staged_cluster_size(long long V) {
   if (forced > 0) return forced;
   if (V <= kStagedMaxV) return 1;
   const long long c = (V + kClusterSlice - 1) / kClusterSlice;
-  return (int)std::min<long long>(c, 16);
+  return c > 10 ? 16 : (int)c;
 }
 
 template <int ALG>
