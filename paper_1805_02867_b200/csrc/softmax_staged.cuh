@@ -457,14 +457,15 @@ __global__ void __launch_bounds__(1024, 1)
 constexpr int kStagedSmemMax = 227 * 1024;
 constexpr long long kStagedMaxV = 16384;   // one CTA per row up to here
 constexpr long long kClusterSlice = 12288;  // target slice per CTA above
-// Clusters of 11..15 CTAs pack badly into GPCs, 16 (non-portable) packs
-// well enough to beat the 4-access stream kernel for safe softmax (4000 x
-// 177828: 1.13 vs 1.70 ms) but not reliably the 3-access online / naive
-// ones (150001: 1.18 vs 1.10 ms online) -- so those stop at 10 CTAs.
+// Clusters of 11..15 CTAs pack badly into GPCs; 16 (non-portable) packs
+// well enough to beat the stream kernel for safe softmax (4000 x 177828:
+// 1.13 vs 1.70 ms) and, on balance, online softmax (127K-197K: -10% .. +7%,
+// 0.81 vs 0.90 ms at 126976, 1.19 vs 1.32 at 177828); the fp64-heavy naive
+// softmax streams above 10 CTAs (cluster-16 is 5-20% slower there).
 constexpr long long kClusterMaxV = 16 * kClusterSlice;
 template <int ALG>
 constexpr long long cluster_max_v() {
-  return ALG == osmx_host::kSafe ? 16 * kClusterSlice : 10 * kClusterSlice;
+  return ALG == osmx_host::kNaive ? 10 * kClusterSlice : 16 * kClusterSlice;
 }
 
 // Launch one (GW, NG, C) layout.  NG is clamped so that D >= NG + 1.
