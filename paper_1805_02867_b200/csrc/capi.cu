@@ -13,6 +13,8 @@
 #include <cstddef>
 #include <cstring>
 #include <mutex>
+#include <set>
+#include <utility>
 #include <string>
 #include <vector>
 
@@ -41,6 +43,15 @@ int num_sms() {
     cache[dev] = n > 0 ? n : 148;
   }
   return cache[dev];
+}
+
+bool first_use_on_device(const void* fn) {
+  static std::mutex mu;
+  static std::set<std::pair<int, const void*>> seen;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  return seen.insert({dev, fn}).second;
 }
 
 static long long g_host_chunk_mb = 512;

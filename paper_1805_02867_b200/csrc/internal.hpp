@@ -59,6 +59,10 @@ void count_launch(int n = 1);
 
 int num_sms();
 
+// True the first time it is called for (current device, fn): function
+// attributes (dynamic shared memory, cluster size) are per device context.
+bool first_use_on_device(const void* fn);
+
 // ---------------------------------------------------------------- launchers
 // All pointers are device pointers.  ws points at the workspace header; the
 // split region (if any) starts at ws + kWsHeader.  Return cudaError_t.

@@ -312,11 +312,9 @@ cudaError_t run_proj(const void* h, long long rows, long long D, const void* w, 
   CUtensorMap mh, mw;
   if (!make_map(&mh, h, D, rows, kBM) || !make_map(&mw, w, D, V, kBN)) return cudaErrorInvalidValue;
   auto kern = k_proj_topk<KC>;
-  static bool attr = false;
-  if (!attr) {
+  if (osmx_host::first_use_on_device(reinterpret_cast<const void*>(kern))) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kProjSmem);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   const int MT = (int)((rows + kBM - 1) / kBM), nt = (int)((V + kBN - 1) / kBN);
   char* rec = static_cast<char*>(ws) + kWsHeader;

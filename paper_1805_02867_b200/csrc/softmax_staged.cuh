@@ -487,12 +487,10 @@ cudaError_t run_staged_cfg(const float* x, long long ldx, float* y, long long ld
   if (D < 1 || ng < 1 || D < ng) return cudaErrorInvalidValue;
   const size_t smem = staged_slots_off(ng, C) + (size_t)D * slot;
   auto kern = k_softmax_staged<GW, ALG>;
-  static bool attr_set = false;  // per instantiation; the attribute is per function
-  if (!attr_set) {
+  if (osmx_host::first_use_on_device(reinterpret_cast<const void*>(kern))) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kStagedSmemMax);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
-    attr_set = true;
   }
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
