@@ -482,14 +482,25 @@ __global__ void __launch_bounds__(32)
   TopList<KC, long long> L;
   L.init(k);
   for (int c = l; c < n; c += 32) {
+    // every field of the record is loaded before any is used (independent
+    // loads in flight together instead of one L2 round trip per field)
     const char* my = rr + (size_t)c * rb;
     const RecHdr h = *reinterpret_cast<const RecHdr*>(my);
+    const float* rv = reinterpret_cast<const float*>(my + rec_vals_off());
+    const long long* ri = reinterpret_cast<const long long*>(my + rec_idx_off(k));
+    float cv[KC];
+    long long ci[KC];
+#pragma unroll
+    for (int r = 0; r < KC; ++r) {
+      cv[r] = r < k ? rv[r] : kNegInf;
+      ci[r] = r < k ? ri[r] : -1LL;
+    }
     a = md_merge(a, MD{h.m, h.d});
     if (h.mn != h.mn) nan_seen = true;
     mn = fminf(mn, h.mn);
-    const float* rv = reinterpret_cast<const float*>(my + rec_vals_off());
-    const long long* ri = reinterpret_cast<const long long*>(my + rec_idx_off(k));
-    for (int r = 0; r < k; ++r) L.offer_ordered(rv[r], ri[r]);
+#pragma unroll
+    for (int r = 0; r < KC; ++r)
+      if (r < k) L.offer_ordered(cv[r], ci[r]);
   }
   a = md_group_reduce<32>(a);
   mn = group_min<32>(mn);
@@ -776,7 +787,10 @@ cudaError_t run_split(const float* x, long long ldx, long long rows, long long V
         char* mid = rec + (size_t)(rows * R) * rec_bytes_(k);
         k_topk_combine_cta<KC, 256><<<dim3((unsigned)rows, (unsigned)G), 256, 0, st>>>(rec, (int)R, k, MODE, mid,
                                                                                     nullptr, nullptr, 0, ws);
-        k_topk_combine_cta<KC, 256><<<(unsigned)rows, 256, 0, st>>>(mid, G, k, MODE, out_rec, vals, idx, 0, ws);
+        if (G <= 64)  // one warp: no cross-warp merge on the last, tiny level
+          k_topk_combine<KC><<<(unsigned)rows, 32, 0, st>>>(mid, G, k, MODE, out_rec, vals, idx, 0, ws);
+        else
+          k_topk_combine_cta<KC, 256><<<(unsigned)rows, 256, 0, st>>>(mid, G, k, MODE, out_rec, vals, idx, 0, ws);
         osmx_host::count_launch();
       } else if (R >= 64) {
         k_topk_combine_cta<KC, 256><<<(unsigned)rows, 256, 0, st>>>(rec, (int)R, k, MODE, out_rec, vals, idx, 0, ws);
