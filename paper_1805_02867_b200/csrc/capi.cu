@@ -338,6 +338,9 @@ osmx_status osmx_config_set(const char* key, int64_t value) {
   } else if (!strcmp(key, "split_cta")) {
     if (value < 0 || value > 1) return OSMX_ERR_INVALID_ARG;
     t.split_cta = (int)value;
+  } else if (!strcmp(key, "proj_bn")) {
+    if (value != 0 && value != 128 && value != 256) return OSMX_ERR_INVALID_ARG;
+    t.proj_bn = (int)value;
   } else if (!strcmp(key, "topk_pipe")) {
     if (value < 0 || value > 6) return OSMX_ERR_INVALID_ARG;
     t.topk_pipe = (int)value;
@@ -371,6 +374,7 @@ int64_t osmx_config_get(const char* key) {
   if (!strcmp(key, "l2_prefetch")) return t.l2_prefetch;
   if (!strcmp(key, "topk_u8")) return t.topk_u8;
   if (!strcmp(key, "topk_pipe")) return t.topk_pipe;
+  if (!strcmp(key, "proj_bn")) return t.proj_bn;
   if (!strcmp(key, "split_cta")) return t.split_cta;
   if (!strcmp(key, "stream_ctas")) return t.stream_ctas;
   if (!strcmp(key, "staged_gw")) return t.staged_gw;

@@ -46,6 +46,7 @@ struct Tuning {
   int staged_ng = 0;            // staged softmax: row groups per CTA (0 auto; clamped to the slots)
   int staged_kb = 0;            // staged softmax: ring (shared memory) per CTA, KB (0 auto)
   int split_cta = 0;            // top-K split path: 0 warp-per-piece records, 1 CTA-per-chunk (legacy)
+  int proj_bn = 0;              // fused projection vocabulary tile (0 auto; 128, 256)
   int topk_pipe = 0;            // warp-per-row top-K via a cp.async smem pipeline (0 off; 1..3 layouts)
   int topk_u8 = -1;             // warp-per-row top-K with 8 float4s in flight (-1 auto)
   int l2_prefetch = -1;         // bulk L2 prefetch distance in batches (0 off, -1 auto)

@@ -32,13 +32,18 @@ using namespace osmx_dev;
 
 namespace {
 
-constexpr int kBM = 128, kBN = 256, kBK = 64;  // tile, K-stage (64 bf16 = one 128-byte swizzle row)
-constexpr int kStages = 4;
+constexpr int kBM = 128, kBK = 64;  // row tile, K-stage (64 bf16 = one 128-byte swizzle row)
 constexpr int kABytes = kBM * kBK * 2;  // 16 KB
-constexpr int kBBytes = kBN * kBK * 2;  // 32 KB
-constexpr int kStageBytes = kABytes + kBBytes;
 constexpr int kProjThreads = 256;
-constexpr size_t kProjSmem = 1024 /* align slack */ + (size_t)kStages * kStageBytes + 256;
+// BN (vocabulary tile) = 256, or 128 for few row tiles (finer load balance)
+template <int BN>
+struct ProjCfg {
+  static constexpr int kStages = BN == 128 ? 6 : 4;  // ~192 KB ring either way
+  static constexpr int kBBytes = BN * kBK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr size_t kSmem = 1024 /* align slack */ + (size_t)kStages * kStageBytes + 256;
+};
+constexpr int kBNMax = 256;
 
 // Bounded mbarrier wait: a protocol bug traps instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait_b(uint64_t* bar, uint32_t parity) {
@@ -78,20 +83,24 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
   return d;
 }
 
-// Instruction descriptor: BF16 x BF16 -> F32, both K-major, M 128, N 256
+// Instruction descriptor: BF16 x BF16 -> F32, both K-major, M 128, N = BN
 // (cute/arch/mma_sm100_desc.hpp InstrDescriptor).
-constexpr uint32_t kIdesc = (1u << 4)            // c_format F32
-                            | (1u << 7)          // a_format BF16
-                            | (1u << 10)         // b_format BF16
-                            | ((uint32_t)(kBN >> 3) << 17)  // n_dim
-                            | ((uint32_t)(kBM >> 4) << 24); // m_dim
+template <int BN>
+constexpr uint32_t idesc_bf16() {
+  return (1u << 4)                        // c_format F32
+         | (1u << 7)                      // a_format BF16
+         | (1u << 10)                     // b_format BF16
+         | ((uint32_t)(BN >> 3) << 17)    // n_dim
+         | ((uint32_t)(kBM >> 4) << 24);  // m_dim
+}
 
+template <int BN>
 __device__ __forceinline__ void umma_bf16(uint32_t tmem_c, uint64_t adesc, uint64_t bdesc, uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_c),
-      "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(acc)
+      "l"(adesc), "l"(bdesc), "r"(idesc_bf16<BN>()), "r"(acc)
       : "memory");
 }
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
@@ -105,11 +114,14 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
 // fills one while the epilogue warps drain the other, and the TMA producer
 // runs ahead across tile boundaries -- the epilogue and the pipeline fill
 // are hidden behind the tensor-core mainloop.
-template <int KC>
+template <int KC, int BN>
 __global__ void __launch_bounds__(kProjThreads, 1)
     k_proj_topk(const __grid_constant__ CUtensorMap tmap_h, const __grid_constant__ CUtensorMap tmap_w, int rows,
                 int D, int V, int k, char* __restrict__ rec, int MT, int NT) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
+  constexpr int kBN = BN;
+  constexpr int kStageBytes = ProjCfg<BN>::kStageBytes;
+  constexpr int kStages = ProjCfg<BN>::kStages;
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
   uint64_t* empty = full + kStages;
@@ -176,7 +188,7 @@ __global__ void __launch_bounds__(kProjThreads, 1)
         const uint64_t ad = umma_desc_sw128(a), bd = umma_desc_sw128(a + kABytes);
 #pragma unroll
         for (int kk = 0; kk < kBK / 16; ++kk)  // K 16 per MMA = 32 bytes along the swizzled row
-          umma_bf16(acc_t, ad + (uint64_t)((kk * 32) >> 4), bd + (uint64_t)((kk * 32) >> 4), (kc | kk) != 0);
+          umma_bf16<BN>(acc_t, ad + (uint64_t)((kk * 32) >> 4), bd + (uint64_t)((kk * 32) >> 4), (kc | kk) != 0);
         umma_commit(&empty[s]);  // stage free once these MMAs have read it
       }
       umma_commit(&afull[b]);  // accumulator b complete
@@ -306,21 +318,22 @@ bool make_map(CUtensorMap* m, const void* base, long long inner, long long outer
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int KC>
-cudaError_t run_proj(const void* h, long long rows, long long D, const void* w, long long V, int k, float* vals,
-                     long long* idx, void* ws, cudaStream_t st) {
+template <int KC, int BN>
+cudaError_t run_proj_bn(const void* h, long long rows, long long D, const void* w, long long V, int k, float* vals,
+                        long long* idx, void* ws, cudaStream_t st) {
+  constexpr size_t smem = ProjCfg<BN>::kSmem;
   CUtensorMap mh, mw;
-  if (!make_map(&mh, h, D, rows, kBM) || !make_map(&mw, w, D, V, kBN)) return cudaErrorInvalidValue;
-  auto kern = k_proj_topk<KC>;
+  if (!make_map(&mh, h, D, rows, kBM) || !make_map(&mw, w, D, V, BN)) return cudaErrorInvalidValue;
+  auto kern = k_proj_topk<KC, BN>;
   if (osmx_host::first_use_on_device(reinterpret_cast<const void*>(kern))) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kProjSmem);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  const int MT = (int)((rows + kBM - 1) / kBM), nt = (int)((V + kBN - 1) / kBN);
+  const int MT = (int)((rows + kBM - 1) / kBM), nt = (int)((V + BN - 1) / BN);
   char* rec = static_cast<char*>(ws) + kWsHeader;
   const long long tiles = (long long)MT * nt;
   const int grid = (int)std::min<long long>(tiles, osmx_host::num_sms());
-  kern<<<grid, kProjThreads, kProjSmem, st>>>(mh, mw, (int)rows, (int)D, (int)V, k, rec, MT, nt);
+  kern<<<grid, kProjThreads, smem, st>>>(mh, mw, (int)rows, (int)D, (int)V, k, rec, MT, nt);
   osmx_host::count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
@@ -332,12 +345,27 @@ cudaError_t run_proj(const void* h, long long rows, long long D, const void* w, 
   return cudaGetLastError();
 }
 
+// Vocabulary tile: 256 columns (128 only when forced: measured slower at
+// every tested shape, 32..4096 rows, tools/proj_bench.py -- the finer load
+// balance does not pay for twice the per-tile epilogues and records).
+inline int proj_bn(long long) {
+  const int forced = osmx_host::tuning().proj_bn;
+  return forced ? forced : 256;
+}
+
+template <int KC>
+cudaError_t run_proj(const void* h, long long rows, long long D, const void* w, long long V, int k, float* vals,
+                     long long* idx, void* ws, cudaStream_t st) {
+  if (proj_bn(rows) == 128) return run_proj_bn<KC, 128>(h, rows, D, w, V, k, vals, idx, ws, st);
+  return run_proj_bn<KC, 256>(h, rows, D, w, V, k, vals, idx, ws, st);
+}
+
 }  // namespace
 
 namespace osmx_host {
 
 size_t proj_topk_ws(long long rows, long long V, int k) {
-  const long long nt = (V + kBN - 1) / kBN;
+  const long long nt = (V + 128 - 1) / 128;  // the finer of the two tile widths
   return (size_t)(rows * nt) * rec_bytes_(k);
 }
 

@@ -12,19 +12,25 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
+@pytest.mark.parametrize("bn", [0, 128, 256])
 @pytest.mark.parametrize("rows,D,V,k", [(128, 64, 256, 5), (200, 256, 3000, 5), (129, 520, 4097, 8),
                                         (512, 1024, 32768, 5), (64, 4096, 20000, 32), (300, 128, 700, 1),
                                         (1000, 512, 70000, 5)])
-def test_proj_topk_vs_reference_on_fp32_logits(cuda, oracle_mod, rows, D, V, k):
+def test_proj_topk_vs_reference_on_fp32_logits(cuda, oracle_mod, rows, D, V, k, bn):
     import torch
 
-    from paper_1805_02867_b200 import osmx
+    from paper_1805_02867_b200 import _lib, osmx
+
+    _lib.config_set("proj_bn", bn)
 
     g = torch.Generator(device="cuda")
     g.manual_seed(rows * 7 + V)
     h = (torch.randn((rows, D), device="cuda", generator=g) / D ** 0.25).to(torch.bfloat16)
     w = (torch.randn((V, D), device="cuda", generator=g) / D ** 0.25).to(torch.bfloat16)
-    vals, idx = osmx.proj_softmax_topk(h, w, k)
+    try:
+        vals, idx = osmx.proj_softmax_topk(h, w, k)
+    finally:
+        _lib.config_set("proj_bn", 0)
     z = torch.mm(h, w.t(), out_dtype=torch.float32)
     zc = z.cpu().numpy()
     rv, rz, st = oracle_mod.batch("online_softmax_topk", zc, k=k)
