@@ -827,7 +827,9 @@ bool topk_uses_split(long long rows, long long V) {
   const auto& tn = osmx_host::tuning();
   if (tn.shape == osmx_host::kShapeSplit) return true;
   if (tn.shape != osmx_host::kShapeAuto) return false;
-  return V > 65536 && rows < 2LL * osmx_host::num_sms();
+  // warp-per-piece records beat a CTA per row up to ~3 rows per SM (300 rows:
+  // 1.6x at V = 128K and 1M), not at 1000 rows (CTA per row: 0.10 vs 0.16 ms)
+  return V > 65536 && rows < 3LL * osmx_host::num_sms();
 }
 
 template <int KC>
