@@ -646,11 +646,14 @@ inline int topk_row_threads(long long rows, long long V) {
   // (128 threads) and 5.9 (256); it wins down to ~4000 rows.
   // 4000 rows: warp/row 4.7-7.0 TB/s vs 3.5-6.5 (128 thr); 1000 rows: 128 thr
   // 2.9-4.8 TB/s vs 1.6-2.3 (warp/row) -- tools/shape_sweep.py, cold L2.
-  // Also measured and rejected for the warp-per-row kernel: 8 float4s in
-  // flight (73 regs, -20%), software-pipelined next-batch loads (80 regs,
-  // -20% at 4000 rows: fewer resident warps than rows), a 48/40-register
-  // cap (spills; -0..-30%).
+  // (Those early rejections of deeper per-warp pipelining were for many-row
+  // launches; for one wave of rows the register double-buffered variant is
+  // the default, see run_rows.)
+  // 1184..1775 rows: warp per row (double-buffered) up to V = 64K (1600 x
+  // 32K: 0.058 vs 0.068 ms), a 256-thread CTA per row above (1600 x 1M:
+  // 1.00 vs 1.18 ms for 128 threads); fewer rows: 128-thread CTAs.
   if (V <= 2048 || rows >= 12 * sms) return 32;
+  if (rows >= 8 * sms) return V <= 65536 ? 32 : 256;
   if (rows >= 2 * sms) return 128;
   return 256;
 }
