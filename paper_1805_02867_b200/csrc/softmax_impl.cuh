@@ -491,6 +491,7 @@ __global__ void __launch_bounds__(BLOCK)
   const int S = gridDim.x;
   const long long row = blockIdx.y;
   const int t = threadIdx.x;
+  pdl_wait();  // records come from the part kernel
   const SRec* rr = rec + row * S;
   float M = kNegInf, mn = -kNegInf, r = 0.0f;
   double rd = 0.0;
@@ -688,7 +689,8 @@ cudaError_t run_split(const float* x, long long ldx, float* y, long long ldy, lo
     k_softmax_split_part<kSplitBlock, kSplitU, ALG, 1><<<grid, kSplitBlock, 0, st>>>(x, ldx, V, ch, rec);
     osmx_host::count_launch();
   }
-  k_softmax_split_scale<kSplitBlock, kSplitU, ALG><<<grid, kSplitBlock, 0, st>>>(x, ldx, y, ldy, V, ch, rec, ws);
+  launch_pdl(k_softmax_split_scale<kSplitBlock, kSplitU, ALG>, grid, dim3(kSplitBlock), 0, st, x, ldx, y, ldy, V, ch,
+             (const SRec*)rec, ws);
   osmx_host::count_launch();
   return cudaGetLastError();
 }

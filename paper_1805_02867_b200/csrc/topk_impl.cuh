@@ -472,6 +472,7 @@ __global__ void __launch_bounds__(32)
     k_topk_combine(const char* __restrict__ rec, int n, int k, int mode, char* __restrict__ out_rec,
                    float* __restrict__ vals, long long* __restrict__ idx, long long row_base,
                    void* ws) {
+  pdl_wait();  // records come from the previous kernel
   const long long row = blockIdx.x;
   const int l = threadIdx.x;
   const size_t rb = rec_bytes_(k);
@@ -551,6 +552,7 @@ __global__ void __launch_bounds__(NT)
   __shared__ float smf[2 * NW];
   __shared__ float sv[NW * KC];
   __shared__ long long si[NW * KC];
+  pdl_wait();  // records come from the previous kernel
   const long long row = blockIdx.x;
   const int t = threadIdx.x, l = t & 31, w = t >> 5;
   const size_t rb = rec_bytes_(k);
@@ -788,17 +790,21 @@ cudaError_t run_split(const float* x, long long ldx, long long rows, long long V
         // two levels: G groups of <= 256 records per row, then the G records
         const int G = (int)((R + 255) / 256);
         char* mid = rec + (size_t)(rows * R) * rec_bytes_(k);
-        k_topk_combine_cta<KC, 256><<<dim3((unsigned)rows, (unsigned)G), 256, 0, st>>>(rec, (int)R, k, MODE, mid,
-                                                                                    nullptr, nullptr, 0, ws);
+        launch_pdl(k_topk_combine_cta<KC, 256>, dim3((unsigned)rows, (unsigned)G), dim3(256), 0, st,
+                   (const char*)rec, (int)R, k, (int)MODE, mid, (float*)nullptr, (long long*)nullptr, 0LL, ws);
         if (G <= 64)  // one warp: no cross-warp merge on the last, tiny level
-          k_topk_combine<KC><<<(unsigned)rows, 32, 0, st>>>(mid, G, k, MODE, out_rec, vals, idx, 0, ws);
+          launch_pdl(k_topk_combine<KC>, dim3((unsigned)rows), dim3(32), 0, st, (const char*)mid, G, k, (int)MODE,
+                     out_rec, vals, idx, 0LL, ws);
         else
-          k_topk_combine_cta<KC, 256><<<(unsigned)rows, 256, 0, st>>>(mid, G, k, MODE, out_rec, vals, idx, 0, ws);
+          launch_pdl(k_topk_combine_cta<KC, 256>, dim3((unsigned)rows), dim3(256), 0, st, (const char*)mid, G, k,
+                     (int)MODE, out_rec, vals, idx, 0LL, ws);
         osmx_host::count_launch();
       } else if (R >= 64) {
-        k_topk_combine_cta<KC, 256><<<(unsigned)rows, 256, 0, st>>>(rec, (int)R, k, MODE, out_rec, vals, idx, 0, ws);
+        launch_pdl(k_topk_combine_cta<KC, 256>, dim3((unsigned)rows), dim3(256), 0, st, (const char*)rec, (int)R, k,
+                   (int)MODE, out_rec, vals, idx, 0LL, ws);
       } else
-        k_topk_combine<KC><<<(unsigned)rows, 32, 0, st>>>(rec, (int)R, k, MODE, out_rec, vals, idx, 0, ws);
+        launch_pdl(k_topk_combine<KC>, dim3((unsigned)rows), dim3(32), 0, st, (const char*)rec, (int)R, k, (int)MODE,
+                   out_rec, vals, idx, 0LL, ws);
       osmx_host::count_launch();
       return cudaGetLastError();
     }
