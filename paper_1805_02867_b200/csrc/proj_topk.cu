@@ -338,9 +338,11 @@ cudaError_t run_proj_bn(const void* h, long long rows, long long D, const void* 
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if (nt >= 64)
-    k_topk_combine_cta<KC, 256><<<(unsigned)rows, 256, 0, st>>>(rec, nt, k, kModeFused, nullptr, vals, idx, 0, ws);
+    launch_pdl(k_topk_combine_cta<KC, 256>, dim3((unsigned)rows), dim3(256), 0, st, (const char*)rec, nt, k,
+               (int)kModeFused, (char*)nullptr, vals, idx, 0LL, ws);
   else
-    k_topk_combine<KC><<<(unsigned)rows, 32, 0, st>>>(rec, nt, k, kModeFused, nullptr, vals, idx, 0, ws);
+    launch_pdl(k_topk_combine<KC>, dim3((unsigned)rows), dim3(32), 0, st, (const char*)rec, nt, k, (int)kModeFused,
+               (char*)nullptr, vals, idx, 0LL, ws);
   osmx_host::count_launch();
   return cudaGetLastError();
 }
