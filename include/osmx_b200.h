@@ -168,14 +168,23 @@ void osmx_host_release(void);
 
 /* Number of kernel launches issued by this library since load. */
 uint64_t osmx_launch_count(void);
+/* Diagnostic: a pure read stream over `bytes` (16-byte aligned) -- the
+ * 128-bit grid-stride max-fold the fused top-K's loads reduce to -- so a
+ * bench can state the achievable read bandwidth of the same buffer.
+ * Writes one float to `sink` (device); stream-ordered. */
+osmx_status osmx_diag_read_probe(const void* x, size_t bytes, float* sink, void* stream);
 /* Launch-layer knobs (tuning and measurement only):
- *   "shape"          0 auto, 1 resident, 2 stream, 3 split
+ *   "shape"          0 auto, 1 resident, 2 stream, 3 split, 4 staged, 5 cluster-staged
  *   "resident_max_v" largest V held in registers (<= 16384)
- *   "split_chunk"    elements per CTA in split mode (0 = auto)
+ *   "split_chunk"    elements per CTA / warp piece in split mode (0 = auto)
  *   "stream_threads" CTA size of the stream kernels (0, 256, 512, 1024)
+ *   "stream_ctas"    persistent stream CTAs per SM with evict-last pass 1 (0 = off)
+ *   "staged_gw" / "staged_ng" / "staged_kb" / "cluster_size"   staged layouts (0 = auto)
  *   "topk_threads"   threads per row of the row top-K (0 auto, 32, 128, 256, 512)
+ *   "topk_u8" / "topk_pipe" / "l2_prefetch" / "tma" / "split_cta"   top-K variants
+ *   "proj_bn"        fused projection vocabulary tile (0 auto, 128, 256)
  *   "host_chunk_mb"  staging block of the host path (default 512)
- * Returns OSMX_ERR_INVALID_ARG for an unknown key. */
+ * Returns OSMX_ERR_INVALID_ARG for an unknown key or value. */
 osmx_status osmx_config_set(const char* key, int64_t value);
 int64_t osmx_config_get(const char* key);
 

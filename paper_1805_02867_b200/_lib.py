@@ -49,6 +49,7 @@ SIGNATURES = {
     "osmx_topk_host": (_int, [_vp, _i64, _i64, _i32, _vp, _vp, _int, _pi64]),
     "osmx_host_release": (None, []),
     "osmx_launch_count": (C.c_uint64, []),
+    "osmx_diag_read_probe": (_int, [_vp, _sz, _vp, _vp]),
     "osmx_config_set": (_int, [C.c_char_p, _i64]),
     "osmx_config_get": (_i64, [C.c_char_p]),
 }

@@ -302,6 +302,11 @@ osmx_status osmx_scale_with_record(const float* x, int64_t V, const void* record
 
 uint64_t osmx_launch_count(void) { return g_launches.load(); }
 
+osmx_status osmx_diag_read_probe(const void* x, size_t bytes, float* sink, void* stream) {
+  if (!x || !sink || (reinterpret_cast<uintptr_t>(x) & 15)) return OSMX_ERR_INVALID_ARG;
+  return cuda_status(launch_read_probe(x, bytes, sink, static_cast<cudaStream_t>(stream)));
+}
+
 osmx_status osmx_config_set(const char* key, int64_t value) {
   if (!key) return OSMX_ERR_INVALID_ARG;
   auto& t = tuning();

@@ -112,6 +112,9 @@ size_t proj_topk_ws(long long rows, long long V, int k);
 cudaError_t launch_proj_topk(const void* h, long long rows, long long D, const void* w, long long V, int k,
                              float* vals, long long* idx, void* ws, cudaStream_t st);
 
+// Diagnostic read stream (tools/read_peak.cu's probe), capi.cu osmx_diag_read_probe.
+cudaError_t launch_read_probe(const void* x, size_t bytes, float* sink, cudaStream_t st);
+
 // Largest k served by the register top-K lists (and by split records).
 constexpr int kMaxK = 32;
 

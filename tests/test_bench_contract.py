@@ -42,3 +42,4 @@ def test_our_arm_line():
     assert d["e2e"]["h2d_bytes_per_step"] == 512 * 16384 * 4 and d["e2e"]["consistent"] is True
     assert d["parity"]["indices_bit_exact"] is True and d["parity"]["max_rel_err"] <= 1e-5
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
+    assert r["read_probe_GBps"] > 0 and 0 < r["frac_of_read_probe"] < 1.5
