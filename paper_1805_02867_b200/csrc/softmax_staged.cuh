@@ -456,12 +456,18 @@ __global__ void __launch_bounds__(1024, 1)
 
 constexpr int kStagedSmemMax = 227 * 1024;
 constexpr long long kStagedMaxV = 16384;   // one CTA per row up to here
-constexpr long long kClusterSlice = 12288;  // target slice per CTA above
-// Clusters of 11..15 CTAs pack badly into GPCs; 16 (non-portable) packs
-// well enough to beat the stream kernel for safe softmax (4000 x 177828:
-// 1.13 vs 1.70 ms) and, on balance, online softmax (127K-197K: -10% .. +7%,
-// 0.81 vs 0.90 ms at 126976, 1.19 vs 1.32 at 177828); the fp64-heavy naive
-// softmax streams above 10 CTAs (cluster-16 is 5-20% slower there).
+constexpr long long kClusterSlice = 12288;  // slice per CTA of a 16-CTA cluster
+// Cluster sizes that tile the B200's 18-SM GPCs (2, 3, 4, 6, 9) keep up to
+// 144 SMs busy; a 16-CTA cluster fits once per GPC (112 SMs).  From
+// tools/shape_sweep.py (4000 rows, cluster size x group width,
+// profiles/r01s2_cluster_sweep.md): short slices (<= 7680 elements, 4-warp
+// groups) on the smallest such cluster up to 9 x 7680; then 6 or 9 CTAs with
+// 8-warp groups while the slice leaves three ring slots (150000: 0.80 vs 1.11
+// ms at 16 CTAs; two slots: 165888 at 9 CTAs 1.35 ms); 16 CTAs above
+// (177828: 1.19 vs 1.46 ms at 9).  The fp64-heavy naive softmax streams
+// above 10 x 12288.
+constexpr long long kClusterShortSlice = 7680;
+constexpr int kClusterRingKB = 220;
 constexpr long long kClusterMaxV = 16 * kClusterSlice;
 template <int ALG>
 constexpr long long cluster_max_v() {
@@ -531,8 +537,13 @@ inline int staged_cluster_size(long long V) {
   const int forced = osmx_host::tuning().cluster_size;
   if (forced > 0) return forced;
   if (V <= kStagedMaxV) return 1;
-  const long long c = (V + kClusterSlice - 1) / kClusterSlice;
-  return c > 10 ? 16 : (int)c;
+  for (int c : {2, 3, 4, 6, 9})
+    if (V <= c * kClusterShortSlice) return c;
+  for (int c : {6, 9}) {
+    const size_t slot = (size_t)staged_slot_floats(((V + c - 1) / c + 3) / 4 * 4) * 4;
+    if (staged_slots_off(3, c) + 3 * slot <= (size_t)kClusterRingKB * 1024) return c;
+  }
+  return 16;
 }
 
 template <int ALG>
@@ -547,8 +558,8 @@ cudaError_t run_staged(const float* x, long long ldx, float* y, long long ldy, l
   int gw = osmx_host::tuning().staged_gw;
   // two 100 KB CTAs per SM for short rows (4000 rows: 1778 -> 0.0156 vs 0.0205
   // ms, 3162 -> 0.0207 vs 0.0241), one 220 KB ring above
-  const int kb = (C == 1 && Sv <= 4096) ? 100 : 220;
-  if (gw == 0) gw = Sv <= 1024 ? 1 : Sv <= 4096 ? 2 : 4;
+  const int kb = (C == 1 && Sv <= 4096) ? 100 : kClusterRingKB;
+  if (gw == 0) gw = Sv <= 1024 ? 1 : Sv <= 4096 ? 2 : (C > 1 && Sv > kClusterSlice) ? 8 : 4;
   const int ng = gw == 1 ? 16 : Sv <= 8192 ? 6 : 3;
   switch (gw) {
     case 1: return run_staged_cfg<1, ALG>(x, ldx, y, ldy, rows, V, ws, st, ng, kb, C);

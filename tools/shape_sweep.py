@@ -65,8 +65,16 @@ def main():
                         else:
                             r = lib.osmx_softmax(alg, x[i].data_ptr(), V, y[i].data_ptr(), V, a.rows, V,
                                                  ws.data_ptr(), ws.numel(), st)
-                        assert r == 0
+                        if r != 0:
+                            raise RuntimeError(f"status {r}")
 
+                    try:
+                        launch(0, sp)
+                        torch.cuda.synchronize()
+                    except RuntimeError as e:  # layout not launchable for this V
+                        print(json.dumps({"V": V, "alg": alg_name, key: val, "error": str(e)}), flush=True)
+                        _lib.config_set(key, DEFAULTS.get(key, 0))
+                        continue
                     ms, ms_min = time_rotating(launch, nset, a.reps)
                     gbs = algo_bytes(alg_name, a.rows, V, a.k) / (ms * 1e-3) / 1e9
                     dram = (8 * a.rows * V if not topk else 4 * a.rows * V) / (ms * 1e-3) / 1e9
