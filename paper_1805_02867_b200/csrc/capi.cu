@@ -341,7 +341,7 @@ osmx_status osmx_config_set(const char* key, int64_t value) {
     if (value != 0 && (value < 16 || value > 227)) return OSMX_ERR_INVALID_ARG;
     t.staged_kb = (int)value;
   } else if (!strcmp(key, "split_cta")) {
-    if (value < 0 || value > 1) return OSMX_ERR_INVALID_ARG;
+    if (value < -1 || value > 2) return OSMX_ERR_INVALID_ARG;
     t.split_cta = (int)value;
   } else if (!strcmp(key, "proj_bn")) {
     if (value != 0 && value != 128 && value != 256) return OSMX_ERR_INVALID_ARG;

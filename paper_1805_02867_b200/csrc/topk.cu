@@ -20,7 +20,9 @@ size_t topk_split_ws(int alg, long long rows, long long V, int k) {
   const long long S = (V + ch - 1) / ch;
   const long long pc = topk_piece_chunk(rows, V);
   const long long R = (V + pc - 1) / pc;  // warp-per-piece records (fused / topk_of)
-  // + the first-level records of the two-level combine (R >= 1024)
+  // + the first-level records of the two-level combine (R >= 1024).  The
+  // TMA-ring pieces (split_cta = 2) are never more: >= 16K elements over at
+  // most 28 resident CTAs per SM.
   size_t b = (size_t)(rows * std::max(S, R + (R + 255) / 256)) * rec_bytes_(k);
   if (alg == kSafeFusedTopk) b += ((size_t)(rows * S) * sizeof(SRecView) + 255) / 256 * 256;
   return b;

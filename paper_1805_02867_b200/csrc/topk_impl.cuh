@@ -749,6 +749,18 @@ long long topk_piece_chunk(long long rows, long long V) {
   return (ch + 15) / 16 * 16;
 }
 
+// Piece length of the TMA-ring split path: one piece per resident CTA over
+// the whole problem (at least 16K elements), a multiple of 16.
+long long topk_tma_piece_chunk(long long rows, long long V, int k) {
+  long long ch = osmx_host::tuning().split_chunk;
+  if (ch <= 0) {
+    const long long slots = osmx_host::topk_tma_slots(k);
+    ch = (rows * V + slots - 1) / slots;
+    ch = std::max<long long>(ch, 16384);
+  }
+  return (ch + 15) / 16 * 16;
+}
+
 template <int KC, int MODE>
 cudaError_t run_split(const float* x, long long ldx, long long rows, long long V, int k, float* vals,
                       long long* idx, void* ws, cudaStream_t st, long long col0, char* out_rec) {
@@ -765,7 +777,28 @@ cudaError_t run_split(const float* x, long long ldx, long long rows, long long V
     if (e != cudaSuccess) return e;
   }
   if constexpr (MODE != kModeSafe) {
-    if (osmx_host::tuning().split_cta == 0) {
+    int how = osmx_host::tuning().split_cta;
+    // TMA-ring pieces for one row or little work (B200, tools/runs/g38.sh:
+    // 1 x 1M 0.020 vs 0.027 ms, 8 x 1M 0.025 vs 0.029, 1 x 2^26 0.064 vs
+    // 0.066); warp pieces once there are more rows (64 x 1M: 0.070 vs 0.092).
+    if (how < 0) how = (rows == 1 || rows * V <= (8LL << 20)) ? 2 : 0;
+    if (how == 2) {
+      // One TMA-ring CTA per piece: about one piece per resident CTA over the
+      // whole problem, then one CTA-wide combine per row.
+      const long long pc = topk_tma_piece_chunk(rows, V, k);
+      const long long R = (V + pc - 1) / pc;
+      cudaError_t e = osmx_host::launch_topk_tma_records(MODE, x, ldx, rows * R, V, k, ws, st, (int)R, pc, col0, rec);
+      if (e != cudaSuccess) return e;
+      if (R >= 64)
+        launch_pdl(k_topk_combine_cta<KC, 256>, dim3((unsigned)rows), dim3(256), 0, st, (const char*)rec, (int)R, k,
+                   (int)MODE, out_rec, vals, idx, 0LL, ws);
+      else
+        launch_pdl(k_topk_combine<KC>, dim3((unsigned)rows), dim3(32), 0, st, (const char*)rec, (int)R, k, (int)MODE,
+                   out_rec, vals, idx, 0LL, ws);
+      osmx_host::count_launch();
+      return cudaGetLastError();
+    }
+    if (how == 0) {
       // Warp-per-piece records (the warp-per-row kernel in record mode: one
       // ~16K-element piece per warp, about one wave of warps over the whole
       // problem), then a CTA-wide combine per row.

@@ -91,7 +91,8 @@ struct SumOp {
 template <int NCW, int STAGES, int KC, int MODE>
 __global__ void __launch_bounds__((NCW + 1) * 32)
     k_topk_tma(const float* __restrict__ x, long long ldx, long long rows, long long V, int k,
-               float* __restrict__ vals, long long* __restrict__ idx, void* ws) {
+               float* __restrict__ vals, long long* __restrict__ idx, void* ws, int R = 0, long long chunk = 0,
+               long long col0 = 0, char* __restrict__ rec = nullptr) {
   constexpr int NC = NCW * 32;
   constexpr int U = kChunk / 16 / NC;  // float4s per consumer thread per stage
   static_assert(U >= 1 && U * NC * 16 == kChunk, "chunk must split evenly");
@@ -104,6 +105,17 @@ __global__ void __launch_bounds__((NCW + 1) * 32)
   int* si = reinterpret_cast<int*>(sv + NCW * KC);        // NCW*KC
   int* tsh = si + NCW * KC;                               // 2 (row parity)
 
+  // Record mode (rec != nullptr): "row" p is piece p % R of input row p / R,
+  // columns [r * chunk, min(V, (r + 1) * chunk)), and writes a split record
+  // like k_topk_rows' record mode.
+  auto seg_of = [&](long long row, long long& piece0) {
+    if (rec) {
+      piece0 = (row % R) * chunk;
+      return make_seg(x + (row / R) * ldx + piece0, V - piece0 < chunk ? V - piece0 : chunk);
+    }
+    piece0 = 0;
+    return make_seg(x + row * ldx, V);
+  };
   const int w = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -122,7 +134,8 @@ __global__ void __launch_bounds__((NCW + 1) * 32)
       int s = 0;
       uint32_t ph = 0;
       for (long long row = blockIdx.x; row < rows; row += gridDim.x) {
-        const Seg sg = make_seg(x + row * ldx, V);
+        long long piece0;
+        const Seg sg = seg_of(row, piece0);
         const char* b = reinterpret_cast<const char*>(sg.p + sg.head);
         const long long bytes = sg.nvec * 16;
         for (long long off = 0; off < bytes; off += kChunk) {
@@ -146,7 +159,8 @@ __global__ void __launch_bounds__((NCW + 1) * 32)
   uint32_t ph = 0;
   int it = 0;
   for (long long row = blockIdx.x; row < rows; row += gridDim.x, ++it) {
-    const Seg sg = make_seg(x + row * ldx, V);
+    long long piece0;
+    const Seg sg = seg_of(row, piece0);
     if (t == 0) tsh[(it + 1) & 1] = Pass<KC, U, MODE, NC>::f2o(kNegInf);
     Pass<KC, U, MODE, NC> P;
     P.L.init(k);
@@ -185,58 +199,90 @@ __global__ void __launch_bounds__((NCW + 1) * 32)
     // ---- row epilogue (consumers only)
     float outM = 0.0f, outR = 1.0f;
     bool bad;
+    RecHdr hdr{kNegInf, 0.0f, 0.0f, k};
     if constexpr (MODE == kModeFused) {
       const MD tot = md_group_cta<NCW>(P.acc.finish(), smf);
       const float mn = red_group_cta<NCW>(P.mn, -kNegInf, MinOp(), smf);
       outM = tot.m;
       outR = __frcp_rn(tot.d);
       bad = !(tot.d == tot.d) || !isfinite(tot.m) || mn == kNegInf;
+      hdr = RecHdr{tot.m, tot.d, mn, k};
     } else {
       const float c = red_group_cta<NCW>(P.chk, 0.0f, SumOp(), smf);
       bad = !(c == c);
+      hdr.mn = (c == c) ? 0.0f : c;
     }
+    char* my = rec ? rec + (size_t)row * rec_bytes_(k) : nullptr;
     merge_group_cta<NCW>(P.L, k, sv, si, [&](int r, float v, int i) {
       if ((int)(threadIdx.x & 31) == (r & 31)) {
+        if (my) {
+          reinterpret_cast<float*>(my + rec_vals_off())[r] = v;
+          reinterpret_cast<long long*>(my + rec_idx_off(k))[r] = i < 0 ? -1LL : (long long)i + piece0 + col0;
+          return;
+        }
         float out = v;
         if constexpr (MODE == kModeFused) out = expf(v - outM) * outR;  // kernels.hpp:122
         vals[row * k + r] = out;
         idx[row * k + r] = (long long)i;
       }
     });
-    if (bad && t == 0) flag_bad_row(ws, row);
+    if (my) {
+      if (t == 0) *reinterpret_cast<RecHdr*>(my) = hdr;  // non-finite pieces: flagged by the combine
+    } else if (bad && t == 0) {
+      flag_bad_row(ws, row);
+    }
   }
 }
 
 constexpr int kNCW = 8;
-constexpr int kStages = 3;
+constexpr int kStages = 6;
+
+template <int KC, int MODE>
+size_t tma_smem() {
+  return (size_t)kStages * kChunk + 2 * kStages * sizeof(uint64_t) + 2 * kNCW * sizeof(float) +
+         (size_t)kNCW * KC * (sizeof(float) + sizeof(int)) + 2 * sizeof(int);
+}
+template <int KC, int MODE>
+int tma_per_sm() {
+  static int per_sm = 0;  // per instantiation (same on every sm_100 device)
+  if (per_sm == 0) {
+    auto kern = k_topk_tma<kNCW, kStages, KC, MODE>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tma_smem<KC, MODE>());
+    int n = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, (kNCW + 1) * 32, tma_smem<KC, MODE>());
+    per_sm = n < 1 ? 1 : n;
+  }
+  return per_sm;
+}
 
 template <int KC, int MODE>
 cudaError_t run_tma(const float* x, long long ldx, long long rows, long long V, int k, float* vals,
-                    long long* idx, void* ws, cudaStream_t st) {
+                    long long* idx, void* ws, cudaStream_t st, int R = 0, long long chunk = 0, long long col0 = 0,
+                    char* rec = nullptr) {
   auto kern = k_topk_tma<kNCW, kStages, KC, MODE>;
-  const size_t smem = (size_t)kStages * kChunk + 2 * kStages * sizeof(uint64_t) + 2 * kNCW * sizeof(float) +
-                      (size_t)kNCW * KC * (sizeof(float) + sizeof(int)) + 2 * sizeof(int);
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  static int per_sm = 0;  // per instantiation (same on every sm_100 device)
-  if (per_sm == 0) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (kNCW + 1) * 32, smem);
-    if (per_sm < 1) per_sm = 1;
+  const size_t smem = tma_smem<KC, MODE>();
+  const int per_sm = tma_per_sm<KC, MODE>();
+  if (osmx_host::first_use_on_device(reinterpret_cast<const void*>(kern))) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
   }
   const long long grid = std::min<long long>(rows, (long long)per_sm * osmx_host::num_sms());
-  kern<<<(unsigned)grid, (kNCW + 1) * 32, smem, st>>>(x, ldx, rows, V, k, vals, idx, ws);
+  kern<<<(unsigned)grid, (kNCW + 1) * 32, smem, st>>>(x, ldx, rows, V, k, vals, idx, ws, R, chunk, col0, rec);
   osmx_host::count_launch();
   return cudaGetLastError();
 }
 
 template <int MODE>
 cudaError_t dispatch_tma(const float* x, long long ldx, long long rows, long long V, int k, float* vals,
-                         long long* idx, void* ws, cudaStream_t st) {
-  if (k <= 1) return run_tma<1, MODE>(x, ldx, rows, V, k, vals, idx, ws, st);
-  if (k <= 5) return run_tma<5, MODE>(x, ldx, rows, V, k, vals, idx, ws, st);
-  if (k <= 8) return run_tma<8, MODE>(x, ldx, rows, V, k, vals, idx, ws, st);
-  if (k <= 16) return run_tma<16, MODE>(x, ldx, rows, V, k, vals, idx, ws, st);
-  return run_tma<32, MODE>(x, ldx, rows, V, k, vals, idx, ws, st);
+                         long long* idx, void* ws, cudaStream_t st, int R = 0, long long chunk = 0,
+                         long long col0 = 0, char* rec = nullptr) {
+#define OSMX_TMA_CASE(KC) return run_tma<KC, MODE>(x, ldx, rows, V, k, vals, idx, ws, st, R, chunk, col0, rec)
+  if (k <= 1) OSMX_TMA_CASE(1);
+  if (k <= 5) OSMX_TMA_CASE(5);
+  if (k <= 8) OSMX_TMA_CASE(8);
+  if (k <= 16) OSMX_TMA_CASE(16);
+  OSMX_TMA_CASE(32);
+#undef OSMX_TMA_CASE
 }
 
 }  // namespace
@@ -247,5 +293,17 @@ cudaError_t launch_topk_tma(int mode, const float* x, long long ldx, long long r
                             float* vals, long long* idx, void* ws, cudaStream_t st) {
   if (mode == kModeFused) return dispatch_tma<kModeFused>(x, ldx, rows, V, k, vals, idx, ws, st);
   return dispatch_tma<kModeTopkOf>(x, ldx, rows, V, k, vals, idx, ws, st);
+}
+long long topk_tma_slots(int k) {
+  const int per_sm = k <= 1 ? tma_per_sm<1, kModeFused>() : k <= 5 ? tma_per_sm<5, kModeFused>()
+                     : k <= 8 ? tma_per_sm<8, kModeFused>() : k <= 16 ? tma_per_sm<16, kModeFused>()
+                     : tma_per_sm<32, kModeFused>();
+  return (long long)per_sm * num_sms();
+}
+cudaError_t launch_topk_tma_records(int mode, const float* x, long long ldx, long long pieces, long long V, int k,
+                                    void* ws, cudaStream_t st, int R, long long chunk, long long col0, char* rec) {
+  if (mode == kModeFused)
+    return dispatch_tma<kModeFused>(x, ldx, pieces, V, k, nullptr, nullptr, ws, st, R, chunk, col0, rec);
+  return dispatch_tma<kModeTopkOf>(x, ldx, pieces, V, k, nullptr, nullptr, ws, st, R, chunk, col0, rec);
 }
 }  // namespace osmx_host

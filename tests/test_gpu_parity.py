@@ -29,6 +29,10 @@ TOPK_VARIANTS = {
     "warp_bulk": [("topk_threads", 32), ("topk_pipe", 6)],
     "split_cta": [("shape", 3), ("split_chunk", 2048), ("split_cta", 1)],
     "split_auto": [("shape", 3)],
+    "split_warp": [("shape", 3), ("split_chunk", 2048), ("split_cta", 0)],
+    "split_warp_auto": [("shape", 3), ("split_cta", 0)],
+    "split_tma": [("shape", 3), ("split_cta", 2)],
+    "split_tma_small": [("shape", 3), ("split_chunk", 2048), ("split_cta", 2)],
 }
 
 
@@ -39,7 +43,7 @@ def lib():
     _lib.load()
     yield _lib
     for key, val in (("shape", 0), ("split_chunk", 0), ("tma", 0), ("topk_threads", 0), ("topk_u8", -1),
-                     ("l2_prefetch", -1), ("cluster_size", 0), ("topk_pipe", 0), ("split_cta", 0)):
+                     ("l2_prefetch", -1), ("cluster_size", 0), ("topk_pipe", 0), ("split_cta", -1)):
         _lib.config_set(key, val)
 
 

@@ -1,0 +1,5 @@
+for r in 1 8 64 256; do
+  timeout 300 python tools/shape_sweep.py --rows $r --alg online_fused --V 1048576 4194304 --knob split_cta=0,2 --reps 9 2>&1 | grep -E "^\{" | sed "s/^/rows$r /"
+done
+timeout 300 python tools/c5_sweep.py split_cta=0 split_cta=2 2>&1 | tail -2
+timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -k "split or topk" 2>&1 | tail -2

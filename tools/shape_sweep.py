@@ -20,7 +20,7 @@ import torch  # noqa: E402
 from bench import algo_bytes, n_rotating_sets, time_rotating  # noqa: E402
 from paper_1805_02867_b200 import _lib  # noqa: E402
 
-DEFAULTS = {"resident_max_v": 2048, "tma": 0, "topk_u8": -1, "l2_prefetch": -1, "topk_pipe": 0, "split_cta": 0, "staged_kb": 0, "staged_gw": 0, "staged_ng": 0, "stream_ctas": 0, "cluster_size": 0, "stream_threads": 0}
+DEFAULTS = {"resident_max_v": 2048, "tma": 0, "topk_u8": -1, "l2_prefetch": -1, "topk_pipe": 0, "split_cta": -1, "staged_kb": 0, "staged_gw": 0, "staged_ng": 0, "stream_ctas": 0, "cluster_size": 0, "stream_threads": 0}
 IDS = {"naive": 0, "safe": 1, "online": 2, "safe_unfused": 3, "safe_fused": 4, "online_fused": 5,
        "online_unfused": 6}
 
