@@ -778,10 +778,11 @@ cudaError_t run_split(const float* x, long long ldx, long long rows, long long V
   }
   if constexpr (MODE != kModeSafe) {
     int how = osmx_host::tuning().split_cta;
-    // TMA-ring pieces for one row or little work (B200, tools/runs/g38.sh:
-    // 1 x 1M 0.020 vs 0.027 ms, 8 x 1M 0.025 vs 0.029, 1 x 2^26 0.064 vs
-    // 0.066); warp pieces once there are more rows (64 x 1M: 0.070 vs 0.092).
-    if (how < 0) how = (rows == 1 || rows * V <= (8LL << 20)) ? 2 : 0;
+    // TMA-ring pieces for one row (B200, tools/runs/g38.sh, g39.sh: 1 x 1M
+    // 0.020 vs 0.027 ms, 1 x 4M 0.023 vs 0.029, 1 x 2^26 0.063 vs 0.067);
+    // warp pieces once there are more rows (8 x 4M: 0.042 vs 0.056, 64 x 1M:
+    // 0.070 vs 0.092).
+    if (how < 0) how = (rows == 1 || rows * V <= (2LL << 20)) ? 2 : 0;
     if (how == 2) {
       // One TMA-ring CTA per piece: about one piece per resident CTA over the
       // whole problem, then one CTA-wide combine per row.

@@ -23,6 +23,7 @@
 namespace {
 
 constexpr int kChunk = 16384;  // bytes per stage (4096 floats)
+constexpr int kTmaMinBlocks = 3;  // 3 CTAs (24 consumer warps) per SM: <= 72 registers
 
 // Consumer-group reductions over NC threads using named barrier 1.
 template <int NCW>
@@ -89,7 +90,7 @@ struct SumOp {
 };
 
 template <int NCW, int STAGES, int KC, int MODE>
-__global__ void __launch_bounds__((NCW + 1) * 32)
+__global__ void __launch_bounds__((NCW + 1) * 32, kTmaMinBlocks)
     k_topk_tma(const float* __restrict__ x, long long ldx, long long rows, long long V, int k,
                float* __restrict__ vals, long long* __restrict__ idx, void* ws, int R = 0, long long chunk = 0,
                long long col0 = 0, char* __restrict__ rec = nullptr) {
@@ -235,7 +236,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32)
 }
 
 constexpr int kNCW = 8;
-constexpr int kStages = 6;
+constexpr int kStages = 4;  // 3 x 4 x 16 KB of ring per SM
 
 template <int KC, int MODE>
 size_t tma_smem() {
