@@ -159,11 +159,15 @@ struct L2Acc {
   __device__ __forceinline__ void add_batch(const float4 (&v)[U]) {
     float s = 0.0f;
     if (!huge) {
+      // paired FFMA2 / FADD2 (sm_100): the same roundings as the scalar
+      // fmaf(x, L, -n) terms and (a + b) + (c + e) sums, half the issue slots
+      const float2 L2 = make_float2(kLog2e, kLog2e), N2 = make_float2(-n, -n);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const float a = ex2(fmaf(v[u].x, kLog2e, -n)), b = ex2(fmaf(v[u].y, kLog2e, -n));
-        const float c = ex2(fmaf(v[u].z, kLog2e, -n)), e = ex2(fmaf(v[u].w, kLog2e, -n));
-        s += (a + b) + (c + e);
+        const float2 t0 = __ffma2_rn(make_float2(v[u].x, v[u].y), L2, N2);
+        const float2 t1 = __ffma2_rn(make_float2(v[u].z, v[u].w), L2, N2);
+        const float2 p = __fadd2_rn(make_float2(ex2(t0.x), ex2(t1.x)), make_float2(ex2(t0.y), ex2(t1.y)));
+        s += p.x + p.y;  // (a + b) + (c + e)
       }
     } else {
 #pragma unroll
