@@ -18,6 +18,8 @@ cases = [
     ("resident", {"shape": 1}, [(7, 100), (5, 1023), (3, 2045)]),
     ("staged", {"shape": 4}, [(300, 3001), (40, 16383)]),
     ("cluster", {"shape": 5, "cluster_size": 4}, [(40, 70001), (9, 5)]),
+    ("cluster9", {"shape": 5, "cluster_size": 9}, [(20, 150001)]),
+    ("cluster_auto", {"shape": 5}, [(20, 100001)]),
     ("stream", {"shape": 2}, [(3, 40001)]),
     ("split", {"shape": 3, "split_chunk": 4096}, [(2, 50001)]),
 ]
@@ -47,6 +49,10 @@ x = dev(rng.standard_normal((3, 5000)).astype(np.float32))
 osmx.softmax_topk(x, 100)  # large k
 osmx.topk(x, 5000)
 x1 = dev(rng.standard_normal((1, 300000)).astype(np.float32))
+osmx.softmax_topk(x1, 5)  # one row: TMA-ring pieces + combine
+_lib.config_set("split_cta", 0)
 osmx.softmax_topk(x1, 5)  # warp-piece split + combine
+osmx.topk(x1, 9)
+_lib.config_set("split_cta", -1)
 torch.cuda.synchronize()
 print("sanitize run ok")
