@@ -182,7 +182,7 @@ osmx_status osmx_diag_read_probe(const void* x, size_t bytes, float* sink, void*
  *   "staged_gw" / "staged_ng" / "staged_kb" / "cluster_size"   staged layouts (0 = auto)
  *   "topk_threads"   threads per row of the row top-K (0 auto, 32, 128, 256, 512)
  *   "topk_u8" / "topk_pipe" / "l2_prefetch" / "tma" / "split_cta"   top-K variants
- *   "proj_bn"        fused projection vocabulary tile (0 auto, 128, 256)
+ *   "proj_bn"        fused projection vocabulary tile (0 auto, 128, 224, 256)
  *   "host_chunk_mb"  staging block of the host path (default 512)
  * Returns OSMX_ERR_INVALID_ARG for an unknown key or value. */
 osmx_status osmx_config_set(const char* key, int64_t value);

@@ -344,7 +344,7 @@ osmx_status osmx_config_set(const char* key, int64_t value) {
     if (value < -1 || value > 2) return OSMX_ERR_INVALID_ARG;
     t.split_cta = (int)value;
   } else if (!strcmp(key, "proj_bn")) {
-    if (value != 0 && value != 128 && value != 256) return OSMX_ERR_INVALID_ARG;
+    if (value != 0 && value != 128 && value != 224 && value != 256) return OSMX_ERR_INVALID_ARG;
     t.proj_bn = (int)value;
   } else if (!strcmp(key, "topk_pipe")) {
     if (value < 0 || value > 6) return OSMX_ERR_INVALID_ARG;

@@ -35,10 +35,13 @@ namespace {
 constexpr int kBM = 128, kBK = 64;  // row tile, K-stage (64 bf16 = one 128-byte swizzle row)
 constexpr int kABytes = kBM * kBK * 2;  // 16 KB
 constexpr int kProjThreads = 256;
-// BN (vocabulary tile) = 256, or 128 for few row tiles (finer load balance)
+// BN (vocabulary tile) = 256, 224 (whole waves of tiles over the SMs when
+// there are few row tiles), or 128 (forced only)
 template <int BN>
 struct ProjCfg {
-  static constexpr int kStages = BN == 128 ? 6 : 4;  // ~192 KB ring either way
+  static constexpr int kStages = BN == 128 ? 6 : 4;  // ~176-192 KB ring
+  // TMEM columns for the two accumulators (allocation: a power of two)
+  static constexpr int kTmemCols = 2 * BN <= 256 ? 256 : 512;
   static constexpr int kBBytes = BN * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr size_t kSmem = 1024 /* align slack */ + (size_t)kStages * kStageBytes + 256;
@@ -148,7 +151,7 @@ __global__ void __launch_bounds__(kProjThreads, 1)
   }
   if (warp == 2) {  // TMEM: 2 x 256 fp32 columns x 128 lanes
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(2 * kBN)
+                 "r"(ProjCfg<BN>::kTmemCols)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -285,7 +288,7 @@ __global__ void __launch_bounds__(kProjThreads, 1)
   __syncthreads();
   if (warp == 2) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * kBN) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ProjCfg<BN>::kTmemCols) : "memory");
   }
 }
 
@@ -347,18 +350,30 @@ cudaError_t run_proj_bn(const void* h, long long rows, long long D, const void* 
   return cudaGetLastError();
 }
 
-// Vocabulary tile: 256 columns (128 only when forced: measured slower at
-// every tested shape, 32..4096 rows, tools/proj_bench.py -- the finer load
-// balance does not pay for twice the per-tile epilogues and records).
-inline int proj_bn(long long) {
+// Vocabulary tile: 256 columns, or 224 when that fills the last wave of the
+// persistent grid clearly better (> 3% shorter waves x width; few row
+// tiles: 128 x 4096 x 131072 has 512 tiles of 256 = 3.46 waves over 148
+// SMs, 586 of 224 = 3.96).  128
+// only when forced: measured slower at every tested shape, 32..4096 rows,
+// tools/proj_bench.py -- the finer load balance does not pay for twice the
+// per-tile epilogues and records.
+inline long long proj_span(long long rows, long long V, int bn) {  // waves x tile width
+  const long long sms = osmx_host::num_sms();
+  const long long tiles = ((rows + kBM - 1) / kBM) * ((V + bn - 1) / bn);
+  return (tiles + sms - 1) / sms * bn;
+}
+inline int proj_bn(long long rows, long long V) {
   const int forced = osmx_host::tuning().proj_bn;
-  return forced ? forced : 256;
+  if (forced) return forced;
+  return proj_span(rows, V, 224) * 103 < proj_span(rows, V, 256) * 100 ? 224 : 256;
 }
 
 template <int KC>
 cudaError_t run_proj(const void* h, long long rows, long long D, const void* w, long long V, int k, float* vals,
                      long long* idx, void* ws, cudaStream_t st) {
-  if (proj_bn(rows) == 128) return run_proj_bn<KC, 128>(h, rows, D, w, V, k, vals, idx, ws, st);
+  const int bn = proj_bn(rows, V);
+  if (bn == 128) return run_proj_bn<KC, 128>(h, rows, D, w, V, k, vals, idx, ws, st);
+  if (bn == 224) return run_proj_bn<KC, 224>(h, rows, D, w, V, k, vals, idx, ws, st);
   return run_proj_bn<KC, 256>(h, rows, D, w, V, k, vals, idx, ws, st);
 }
 

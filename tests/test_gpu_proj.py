@@ -12,7 +12,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("bn", [0, 128, 256])
+@pytest.mark.parametrize("bn", [0, 128, 224, 256])
 @pytest.mark.parametrize("rows,D,V,k", [(128, 64, 256, 5), (200, 256, 3000, 5), (129, 520, 4097, 8),
                                         (512, 1024, 32768, 5), (64, 4096, 20000, 32), (300, 128, 700, 1),
                                         (1000, 512, 70000, 5)])
