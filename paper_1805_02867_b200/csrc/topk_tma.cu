@@ -173,7 +173,22 @@ __global__ void __launch_bounds__((NCW + 1) * 32, kTmaMinBlocks)
       const int n4 = (int)((bytes - off < kChunk ? bytes - off : kChunk) >> 4);
       mbar_wait(&full[s], ph);
       const float4* sb = ring + (size_t)s * (kChunk / 16);
+      const int j0 = sg.head + (int)(off >> 2) + 4 * t;
       float4 v[U];
+      if (n4 == kChunk / 16) {
+        // full stage (every stage but a piece's last): no bounds checks, and
+        // batch_j inlines with a constant count (no per-u masking)
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = sb[t + u * NC];
+        __syncwarp();
+        if ((t & 31) == 0) mbar_arrive(&empty[s]);
+        if (++s == STAGES) {
+          s = 0;
+          ph ^= 1;
+        }
+        P.batch_j(v, U, j0, 4 * NC);
+        continue;
+      }
       int cnt = 0;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -191,7 +206,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, kTmaMinBlocks)
         s = 0;
         ph ^= 1;
       }
-      P.batch_j(v, cnt, sg.head + (int)(off >> 2) + 4 * t, 4 * NC);  // warp-uniform call
+      P.batch_j(v, cnt, j0, 4 * NC);  // warp-uniform call
     }
     if (t < sg.tail) {
       const int j = sg.head + (int)(4 * sg.nvec) + t;
