@@ -749,14 +749,15 @@ long long topk_piece_chunk(long long rows, long long V) {
   return (ch + 15) / 16 * 16;
 }
 
-// Piece length of the TMA-ring split path: one piece per resident CTA over
-// the whole problem (at least 16K elements), a multiple of 16.
+// Piece length of the TMA-ring split path: floor(slots / rows) pieces per
+// row, so that rows x pieces never exceeds the resident CTAs (one wave), at
+// least 16K elements each, a multiple of 16.
 long long topk_tma_piece_chunk(long long rows, long long V, int k) {
   long long ch = osmx_host::tuning().split_chunk;
   if (ch <= 0) {
-    const long long slots = osmx_host::topk_tma_slots(k);
-    ch = (rows * V + slots - 1) / slots;
-    ch = std::max<long long>(ch, 16384);
+    const long long per_row = std::max<long long>(1, osmx_host::topk_tma_slots(k) / std::max<long long>(rows, 1));
+    ch = (V + per_row - 1) / per_row;
+    ch = std::max<long long>((ch + 15) / 16 * 16, 16384);
   }
   return (ch + 15) / 16 * 16;
 }
@@ -778,11 +779,12 @@ cudaError_t run_split(const float* x, long long ldx, long long rows, long long V
   }
   if constexpr (MODE != kModeSafe) {
     int how = osmx_host::tuning().split_cta;
-    // TMA-ring pieces for one row (B200, tools/runs/g38.sh, g39.sh: 1 x 1M
-    // 0.020 vs 0.027 ms, 1 x 4M 0.023 vs 0.029, 1 x 2^26 0.063 vs 0.067);
-    // warp pieces once there are more rows (8 x 4M: 0.042 vs 0.056, 64 x 1M:
-    // 0.070 vs 0.092).
-    if (how < 0) how = (rows == 1 || rows * V <= (2LL << 20)) ? 2 : 0;
+    // TMA-ring pieces (one wave of CTAs, floor(slots / rows) pieces per row)
+    // except for many short rows (B200, tools/runs/g44.sh, g45.sh; ms, TMA
+    // vs warp pieces): 1 x 2^26 0.062 vs 0.067, 8 x 1M 0.026 vs 0.029,
+    // 64 x 1M 0.062 vs 0.068, 400 x 1M 0.270 vs 0.314; but 128 x 256K 0.045
+    // vs 0.038.
+    if (how < 0) how = (rows >= 64 && rows * V <= (1LL << 25)) ? 0 : 2;
     if (how == 2) {
       // One TMA-ring CTA per piece: about one piece per resident CTA over the
       // whole problem, then one CTA-wide combine per row.
