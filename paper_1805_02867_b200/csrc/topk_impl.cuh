@@ -872,9 +872,11 @@ bool topk_uses_split(long long rows, long long V) {
   const auto& tn = osmx_host::tuning();
   if (tn.shape == osmx_host::kShapeSplit) return true;
   if (tn.shape != osmx_host::kShapeAuto) return false;
-  // warp-per-piece records beat a CTA per row up to ~3 rows per SM (300 rows:
-  // 1.6x at V = 128K and 1M), not at 1000 rows (CTA per row: 0.10 vs 0.16 ms)
-  return V > 65536 && rows < 3LL * osmx_host::num_sms();
+  // split records (TMA pieces) beat the row kernels up to ~5 rows per SM
+  // (tools/runs/g46.sh, g47.sh; ms, split vs rows: 444 x 1M 0.30 vs 0.48,
+  // 700 x 1M 0.46 vs 0.54, 444 x 128K 0.054 vs 0.080), not at 1000 rows
+  // (1M: 0.69 vs 0.64; 128K: 0.12 vs 0.10)
+  return V > 65536 && rows < 5LL * osmx_host::num_sms();
 }
 
 template <int KC>

@@ -358,6 +358,30 @@ def test_online_fused_topk_many_rows(cuda, oracle_mod, lib, variant):
         assert max_rel(vals.cpu().numpy(), rv) <= TOL
 
 
+@pytest.mark.parametrize("variant", ["auto", "split_tma", "split_warp_auto"])
+def test_topk_split_more_rows_than_ctas(cuda, oracle_mod, lib, variant):
+    """Split records with more rows than resident CTAs (auto: TMA pieces up to
+    5 rows per SM, one piece per row, CTAs loop over several rows), misaligned
+    rows, fused and topk_of."""
+    from paper_1805_02867_b200 import osmx
+
+    for key, val in TOPK_VARIANTS[variant]:
+        lib.config_set(key, val)
+    rng = np.random.default_rng(13)
+    rows, V = 500, 70001
+    big = dist("normal", rng, rows, V + 1)
+    xt = _dev(big)[:, 1:]  # misaligned rows, ld = V + 1
+    x = np.ascontiguousarray(big[:, 1:])
+    vals, idx = osmx.softmax_topk(xt, 5, alg="online_fused")
+    rv, rz = _topk_ref(oracle_mod, "online_softmax_topk", x, 5)
+    assert np.array_equal(idx.cpu().numpy(), rz), variant
+    assert max_rel(vals.cpu().numpy(), rv) <= TOL
+    tv, ti = osmx.topk(xt, 7)
+    qv, qz = _topk_ref(oracle_mod, "topk_of", x, 7)
+    assert np.array_equal(ti.cpu().numpy(), qz), variant
+    assert np.array_equal(tv.cpu().numpy(), qv)
+
+
 @pytest.mark.parametrize("alg", ["online", "safe", "naive"])
 def test_softmax_cluster_slices(cuda, oracle_mod, lib, alg):
     """Rows split over 2..16 CTAs of a cluster (distributed shared memory

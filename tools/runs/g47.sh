@@ -1,0 +1,4 @@
+for r in 700 850; do
+  timeout 300 python tools/shape_sweep.py --rows $r --alg online_fused --V 131072 1048576 --knob shape=0,3 --reps 7 2>&1 | grep -E "^\{" | sed "s/^/rows$r /"
+done
+timeout 300 python tools/shape_sweep.py --rows 600 --alg online_fused --V 65536 --knob shape=0,3 --reps 7 2>&1 | grep -E "^\{" | sed "s/^/rows600 /"
