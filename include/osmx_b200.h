@@ -181,7 +181,9 @@ osmx_status osmx_diag_read_probe(const void* x, size_t bytes, float* sink, void*
  *   "stream_ctas"    persistent stream CTAs per SM with evict-last pass 1 (0 = off)
  *   "staged_gw" / "staged_ng" / "staged_kb" / "cluster_size"   staged layouts (0 = auto)
  *   "topk_threads"   threads per row of the row top-K (0 auto, 32, 128, 256, 512)
- *   "topk_u8" / "topk_pipe" / "l2_prefetch" / "tma" / "split_cta"   top-K variants
+ *   "topk_u8" / "topk_pipe" / "l2_prefetch" / "tma"   top-K row-kernel variants
+ *   "split_cta"      top-K split records: -1 auto, 0 warp pieces, 1 CTA chunks,
+ *                    2 TMA-ring CTA pieces
  *   "proj_bn"        fused projection vocabulary tile (0 auto, 128, 224, 256)
  *   "host_chunk_mb"  staging block of the host path (default 512)
  * Returns OSMX_ERR_INVALID_ARG for an unknown key or value. */
