@@ -198,18 +198,6 @@ __device__ __forceinline__ MD md_merge(MD a, MD b) {
 // XOR-butterfly over `width` lanes (power of two <= 32): every lane of the
 // group ends with the group total.
 template <int WIDTH>
-__device__ __forceinline__ MD md_group_reduce(MD s) {
-#pragma unroll
-  for (int o = WIDTH / 2; o > 0; o >>= 1) {
-    MD t;
-    t.m = __shfl_xor_sync(0xffffffffu, s.m, o);
-    t.d = __shfl_xor_sync(0xffffffffu, s.d, o);
-    s = md_merge(s, t);
-  }
-  return s;
-}
-
-template <int WIDTH>
 __device__ __forceinline__ float group_max(float v) {
 #pragma unroll
   for (int o = WIDTH / 2; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
@@ -226,6 +214,20 @@ __device__ __forceinline__ float group_sum(float v) {
 #pragma unroll
   for (int o = WIDTH / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
+}
+// (m, d) over a group: the max first, then each lane rescales its own d
+// once (one ex2 per lane instead of two per butterfly step of a merge
+// tree) and a plain sum -- the same poison rules as md_merge (an empty
+// group keeps d's NaN; -inf lanes contribute 0; NaN / +inf poison d).
+template <int WIDTH>
+__device__ __forceinline__ MD md_group_reduce(MD s) {
+  float M = s.m;
+#pragma unroll
+  for (int o = WIDTH / 2; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+  float d = (M == kNegInf) ? s.d : s.d * exp_sub(s.m, M);
+#pragma unroll
+  for (int o = WIDTH / 2; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+  return MD{M, d};
 }
 template <int WIDTH>
 __device__ __forceinline__ double group_sum_d(double v) {
