@@ -64,19 +64,27 @@ __device__ __forceinline__ void tma_load_1d_nohint(void* dst, const void* src, u
 // (2 * GW floats / GW doubles, private to the group).
 template <int GW>
 struct SGrp {
-  __device__ static MD md(MD s, float* sm, int bar_id, int lw) {
+  // (m, d) and the min together: one round of named barriers for both.
+  __device__ static MD md_min(MD s, float& mn, float* sm, int bar_id, int lw) {
     s = md_group_reduce<32>(s);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
     if constexpr (GW == 1) {
       return s;
     } else {
       if ((threadIdx.x & 31) == 0) {
         sm[lw] = s.m;
         sm[GW + lw] = s.d;
+        sm[2 * GW + lw] = mn;
       }
       named_sync(bar_id, GW * 32);
       MD t = MD{sm[0], sm[GW]};
+      mn = sm[2 * GW];
 #pragma unroll
-      for (int i = 1; i < GW; ++i) t = md_merge(t, MD{sm[i], sm[GW + i]});
+      for (int i = 1; i < GW; ++i) {
+        t = md_merge(t, MD{sm[i], sm[GW + i]});
+        mn = fminf(mn, sm[2 * GW + i]);
+      }
       named_sync(bar_id, GW * 32);
       return t;
     }
@@ -309,8 +317,7 @@ __global__ void __launch_bounds__(1024, 1)
           acc.raise(bm);
           if (bm != kNegInf) acc.add_batch<1>(v);
         }
-        MD tot = SGrp<GW>::md(acc.finish(), scr, bar_id, lw);
-        mn = SGrp<GW>::red(mn, SOpMin(), scr, bar_id, lw);
+        MD tot = SGrp<GW>::md_min(acc.finish(), mn, scr, bar_id, lw);
         if (C > 1) {
           const SRecX* rec = exchange(0, SRecX{tot.m, mn, (double)tot.d});
           tot = md_identity();
