@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(kProjThreads, 1)
           if (n0 + c + 4 * j + 3 < V) bn = fminf(bn, fminf(fminf(v[j].x, v[j].y), fminf(v[j].z, v[j].w)));
         }
         mn = fminf(mn, bn);
-        if (bm != kNegInf) {
+        if (n0 + c < V) {  // any real column: added even when the max is -inf, so NaN logits poison d
           acc.raise(bm);
           acc.add_batch<8>(v);
         }

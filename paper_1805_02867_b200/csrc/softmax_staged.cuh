@@ -304,18 +304,33 @@ __global__ void __launch_bounds__(1024, 1)
           acc.raise(bm);
           acc.add_batch<U>(v);
         }
-        for (; q < qb; q += GT) {
-          float4 v[1] = {sl4[q]};
-          mn = min4(mn, v[0]);
-          acc.raise(max4(kNegInf, v[0]));
-          acc.add_batch<1>(v);
+        if (q < qb) {
+          // last partial batch as one masked batch (one raise): the -inf fill
+          // adds e^-inf = 0 terms (every batch is added: a NaN must poison d
+          // even when the batch max, which fmaxf takes past NaN, is -inf)
+          float4 v[U];
+          float bm = kNegInf;
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            if (q + u * GT < qb) {
+              v[u] = sl4[q + u * GT];
+              mn = min4(mn, v[u]);
+            } else {
+              v[u] = make_float4(kNegInf, kNegInf, kNegInf, kNegInf);
+            }
+            bm = max4(bm, v[u]);
+          }
+          acc.raise(bm);
+          acc.add_batch<U>(v);
         }
         if (my_edge >= 0) {
           float4 v[1] = {masked(my_edge, kNegInf)};
           mn = min4(mn, masked(my_edge, -kNegInf));
-          const float bm = max4(kNegInf, v[0]);
-          acc.raise(bm);
-          if (bm != kNegInf) acc.add_batch<1>(v);
+          // always added: a NaN edge element must poison d (max4 and min4
+          // both step past NaN); an all -inf batch on an empty accumulator
+          // poisons it too, and such a row is non-finite anyway
+          acc.raise(max4(kNegInf, v[0]));
+          acc.add_batch<1>(v);
         }
         MD tot = SGrp<GW>::md_min(acc.finish(), mn, scr, bar_id, lw);
         if (C > 1) {

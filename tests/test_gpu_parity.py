@@ -310,6 +310,38 @@ def test_nonfinite_rows_flagged(cuda, lib):
         osmx.softmax(_dev(rng.standard_normal((2, 50)).astype(np.float32)))
 
 
+@pytest.mark.parametrize("shape", ["auto", "resident", "stream", "split", "staged", "cluster"])
+def test_nonfinite_at_row_edges(cuda, lib, shape):
+    """A single NaN / +inf / -inf at the first or last elements of one row,
+    rows at every 16-byte phase (the masked head / tail float4s): that row
+    is the one reported."""
+    from paper_1805_02867_b200 import osmx
+
+    lib.config_set("shape", SHAPES[shape])
+    lib.config_set("split_chunk", 1024 if shape == "split" else 0)
+    lib.config_set("cluster_size", 3 if shape == "cluster" else 0)
+    rng = np.random.default_rng(17)
+    V = 3001
+    for phase in range(4):
+        big = rng.standard_normal((3, V + 4)).astype(np.float32)
+        for pos in (0, 1, 2, V - 2, V - 1):
+            for bad in (np.nan, np.inf, -np.inf):
+                b = big.copy()
+                b[1, phase + pos] = bad
+                xt = _dev(b)[:, phase:phase + V]
+                for alg in ("safe", "online"):
+                    with pytest.raises(osmx.NonFiniteError) as e:
+                        osmx.softmax(xt, alg=alg)
+                    assert e.value.row == 1, (shape, phase, pos, bad, alg)
+                for alg in ("online_fused", "safe_fused"):
+                    with pytest.raises(osmx.NonFiniteError) as e:
+                        osmx.softmax_topk(xt, 3, alg=alg)
+                    assert e.value.row == 1, (shape, phase, pos, bad, alg)
+                with pytest.raises(osmx.NonFiniteError) as e:
+                    osmx.topk(xt, 3)
+                assert e.value.row == 1, (shape, phase, pos, bad, "topk_of")
+
+
 def test_argument_errors(cuda, lib):
     from paper_1805_02867_b200 import osmx
 

@@ -46,3 +46,21 @@ def test_proj_topk_vs_reference_on_fp32_logits(cuda, oracle_mod, rows, D, V, k, 
     rel = np.abs(gv.astype(np.float64) - rv) / rv
     assert rel.max() <= 2e-4, rel.max()  # logits differ by fp32 accumulation order (~1e-6 abs)
     print(f"rows {rows} D {D} V {V} k {k}: index rows differing by logit ties: {diff}, max rel {rel.max():.2e}")
+
+
+def test_proj_nan_logit_block_flagged(cuda):
+    """A whole 32-column chunk of NaN logits (NaN rows of W) must still poison
+    the row normalizer: every row is reported non-finite, like the reference
+    on those fp32 logits."""
+    import torch
+
+    from paper_1805_02867_b200 import osmx
+
+    g = torch.Generator(device="cuda")
+    g.manual_seed(5)
+    h = torch.randn((130, 256), device="cuda", generator=g).to(torch.bfloat16)
+    w = torch.randn((1000, 256), device="cuda", generator=g).to(torch.bfloat16)
+    w[64:128] = float("nan")
+    with pytest.raises(osmx.NonFiniteError) as e:
+        osmx.proj_softmax_topk(h, w, 5)
+    assert e.value.row == 0
