@@ -329,11 +329,11 @@ def test_nonfinite_at_row_edges(cuda, lib, shape):
                 b = big.copy()
                 b[1, phase + pos] = bad
                 xt = _dev(b)[:, phase:phase + V]
-                for alg in ("safe", "online"):
+                for alg in ("naive", "safe", "online"):
                     with pytest.raises(osmx.NonFiniteError) as e:
                         osmx.softmax(xt, alg=alg)
                     assert e.value.row == 1, (shape, phase, pos, bad, alg)
-                for alg in ("online_fused", "safe_fused"):
+                for alg in ("online_fused", "safe_fused", "safe_unfused", "online_unfused"):
                     with pytest.raises(osmx.NonFiniteError) as e:
                         osmx.softmax_topk(xt, 3, alg=alg)
                     assert e.value.row == 1, (shape, phase, pos, bad, alg)
