@@ -86,6 +86,58 @@ def measured_peaks() -> dict:
 
 # ----------------------------------------------------------- clock sampler --
 
+class NvmlClockSampler:
+    """SM clock / clock-event reasons sampled every 10 ms through NVML (the
+    library nvidia-smi reads) during the timed region -- no process start-up
+    inside the window, so short regions still get samples."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40, "sw_power_cap": 0x4}
+
+    def __init__(self, gpu_index: int):
+        import pynvml
+
+        self.nv = pynvml
+        pynvml.nvmlInit()
+        self.h = pynvml.nvmlDeviceGetHandleByIndex(gpu_index)
+        self.smax = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+        self.sm: list[float] = []
+        self.mask = 0
+        self.stop_ev = threading.Event()
+        self.thread = None
+
+    def _run(self):
+        nv = self.nv
+        while not self.stop_ev.is_set():
+            try:
+                self.sm.append(float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)))
+                self.mask |= int(nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            except Exception:  # noqa: BLE001 -- a failed sample is skipped
+                pass
+            self.stop_ev.wait(0.01)
+
+    def start(self):
+        self.thread = threading.Thread(target=self._run, daemon=True)
+        self.thread.start()
+
+    def stop(self) -> dict:
+        self.stop_ev.set()
+        if self.thread:
+            self.thread.join(timeout=2)
+        if not self.sm:
+            return {"sm_mhz": None, "sm_max_mhz": self.smax, "reasons": ["no samples"], "samples": 0}
+        reasons = sorted(n for n, b in self.REASONS.items() if self.mask & b)
+        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": self.smax, "reasons": reasons,
+                "samples": len(self.sm), "source": "nvml"}
+
+
+def clock_sampler(gpu_index: int):
+    """NVML sampler when pynvml is importable, else nvidia-smi -lms."""
+    try:
+        return NvmlClockSampler(gpu_index)
+    except Exception:  # noqa: BLE001 -- no NVML: fall back to the CLI
+        return ClockSampler(gpu_index)
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
@@ -272,7 +324,7 @@ def main() -> None:
         from paper_1805_02867_b200 import _lib
 
         lib = _lib.load()
-        ss = ClockSampler(local)
+        ss = clock_sampler(local)
         ss.start()
         sweep = run_sweeps(lib, _lib, dev, torch.cuda.current_stream(dev).cuda_stream, args.sweep_reps,
                            measured_peaks()["hbm_gbs"])
@@ -336,9 +388,10 @@ def main() -> None:
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
-    sampler = ClockSampler(local)
+    sampler = clock_sampler(local)
     sampler.start()
-    time.sleep(0.2)
+    if isinstance(sampler, ClockSampler):
+        time.sleep(0.2)  # nvidia-smi start-up (NVML samples from the first call)
     launches0 = _lib.launch_count()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     t_start = torch.cuda.Event(enable_timing=True)
@@ -441,7 +494,7 @@ def main() -> None:
     if rank == 0 and world == 1 and (args.sweep == "on" or args.sweep == "auto"):
         # x stays allocated: a buffer mapped right after a 34 GB free made the
         # latency-bound top-K ~25% slower (tools/placement_test.py)
-        ss = ClockSampler(local)
+        ss = clock_sampler(local)
         ss.start()
         sweep = run_sweeps(lib, _lib, dev, sp, args.sweep_reps, measured_peaks()["hbm_gbs"])
         sweep["clocks"] = ss.stop()
