@@ -293,7 +293,7 @@ def run_reference_arm(args) -> None:
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--rows", type=int, default=65536, help="rows per GPU (weak scaling)")
@@ -302,6 +302,8 @@ def main() -> None:
     ap.add_argument("--e2e", default="auto", choices=["auto", "on", "off"])
     ap.add_argument("--cpu", default="auto", choices=["auto", "on", "off"])
     ap.add_argument("--sweep-reps", type=int, default=20)
+    ap.add_argument("--detail-out", default=None,
+                    help="write the full result (sweeps, V-split, notes) as JSON to this path")
     ap.add_argument("--sweep-only", action="store_true", help="print only the configs[1]/[2]/[4] sweeps (N=1)")
     ap.add_argument("--vsplit", default="auto", choices=["auto", "on", "off"],
                     help="configs[4] across ranks: one 2^26 row split over the N GPUs, NCCL record all-gather "
@@ -435,7 +437,7 @@ def main() -> None:
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "f32",
-        "data": "synthetic standard-normal fp32 logits (torch normal_ on device), no checkpoint",
+        "data": "synthetic standard-normal fp32 logits (torch normal_ on device)",
         "config": {"workload": "C4 fused online softmax+Top-5 (online_softmax_topk, Alg. 4), rows sharded",
                    "rows_per_gpu": rows, "V": V, "k": k, "parallelism": f"row-shard x{world} (no collective)",
                    "l2": "inputs 34.4 GB/GPU >> 126 MB L2: no flush needed"},
@@ -482,7 +484,9 @@ def main() -> None:
     # ---- e2e through the host-buffer C-ABI entry point (pinned host rows)
     do_e2e = args.e2e == "on" or (args.e2e == "auto")
     if do_e2e:
-        result["e2e"] = e2e_measure(lib, _lib, x, idx, rows, V, k, dev, world, dist, local)
+        e2e = e2e_measure(lib, _lib, x, idx, rows, V, k, dev, world, dist, local, args.steps)
+        if e2e is not None:
+            result["e2e"] = e2e
 
     # ---- CPU baseline (rank 0, N=1)
     if rank == 0 and world == 1 and args.cpu != "off":
@@ -509,9 +513,86 @@ def main() -> None:
         result["vsplit_c5"] = vsplit_measure(dist, dev, world, rank, args.steps, args.warmup)
 
     if rank == 0:
-        print(json.dumps(result), flush=True)
+        emit(result, args.detail_out)
     if dist is not None:
         dist.destroy_process_group()
+
+
+FINAL_LINE_MAX = 2000  # the driver keeps only the tail of stdout: the headline line must stay short
+
+
+def sweep_summary(sweep: dict) -> dict:
+    """The north-star ratios of the sweeps in a few numbers (the full sweep is
+    printed on the line before the headline and written to --detail-out)."""
+    out = {}
+    sm = [r for r in sweep.get("softmax", []) if r["V"] >= 4096]
+    if sm:
+        out["online_frac_min_V4K"] = min(r["online"]["frac"] for r in sm)
+        out["online_over_safe_stream_min_V4K"] = min(r["online_over_safe_stream"] for r in sm)
+        out["online_stream_over_safe_stream_min_V31K"] = min(
+            (r["online_stream_over_safe_stream"] for r in sm if r["V"] >= 31623), default=None)
+    tk = sweep.get("topk", [])
+    if tk:
+        out["fused_over_online_unfused_min"] = min(r["fused_over_online_unfused"] for r in tk)
+        out["fused_frac_min"] = min(r["online_fused"]["frac"] for r in tk)
+    c5 = sweep.get("c5")
+    if c5:
+        out["c5_fused_ms"] = c5["online_fused"]["ms"]
+        out["c5_fused_frac"] = c5["online_fused"]["frac"]
+    c1 = sweep.get("c1_parity")
+    if c1:
+        out["c1_max_rel_err"] = max(c1[f"{a}_max_rel_err"] for a in ("naive", "safe", "online"))
+    return out
+
+
+def emit(result: dict, detail_out: str | None) -> None:
+    """Print the detail (sweeps, V-split, long notes) on an earlier line and to
+    `detail_out`, then the compact headline JSON line (< FINAL_LINE_MAX bytes)
+    as the LAST line of stdout."""
+    detail = {k: result[k] for k in ("sweep", "vsplit_c5") if k in result}
+    detail["roofline"] = result.get("roofline")
+    detail["e2e"] = result.get("e2e")
+    detail["cpu_baseline"] = result.get("cpu_baseline")
+    if detail_out:
+        p = Path(detail_out)
+        p.parent.mkdir(parents=True, exist_ok=True)
+        p.write_text(json.dumps(result, indent=1))
+    print(json.dumps({"detail": detail}), flush=True)
+    line = compact_line(result)
+    print(json.dumps(line, separators=(",", ":")), flush=True)
+
+
+def compact_line(result: dict) -> dict:
+    keep = ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+            "vs_baseline", "dtype", "data", "config", "rows_per_s", "elements_per_s", "gpu_launches")
+    line = {k: result[k] for k in keep if k in result}
+    c = result.get("clocks") or {}
+    line["clocks"] = {k: c.get(k) for k in ("sm_mhz", "sm_max_mhz", "reasons", "samples")}
+    r = result.get("roofline") or {}
+    line["roofline"] = {k: r[k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic", "avg_launch_ms",
+                                          "read_probe_GBps", "frac_of_read_probe") if k in r}
+    e = result.get("e2e")
+    if e:
+        line["e2e"] = {k: e[k] for k in ("value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step", "steps",
+                                         "ms_per_step", "devices", "consistent") if k in e}
+    cb = result.get("cpu_baseline")
+    if cb:
+        line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample") if k in cb}
+    if result.get("parity"):
+        p = result["parity"]
+        line["parity"] = {"rows": p["rows_checked"], "idx_exact": p["indices_bit_exact"],
+                          "max_rel_err": float(f"{p['max_rel_err']:.3g}")}
+    if result.get("sweep"):
+        line["sweep"] = sweep_summary(result["sweep"])
+    if result.get("vsplit_c5"):
+        v = result["vsplit_c5"]
+        line["vsplit_c5"] = {"ranks": v["ranks"], "ms": v["ms"], "GBps": v["GBps"]}
+    # hard bound: drop the optional context before the contract keys
+    for opt in ("sweep", "vsplit_c5", "parity", "elements_per_s"):
+        if len(json.dumps(line, separators=(",", ":"))) <= FINAL_LINE_MAX:
+            break
+        line.pop(opt, None)
+    return line
 
 
 def vsplit_measure(dist, dev, world, rank, steps, warmup) -> dict:
@@ -550,51 +631,68 @@ def vsplit_measure(dist, dev, world, rank, steps, warmup) -> dict:
             "collective": "one all_gather_into_tensor of fixed-size records (NCCL)", "timing": "max over ranks"}
 
 
-def e2e_measure(lib, _lib, x, dev_idx, rows, V, k, dev, world, dist, local) -> dict:
+def e2e_measure(lib, _lib, x, dev_idx, rows, V, k, dev, world, dist, local, steps) -> dict:
+    """The headline metric through the library's host-buffer row sharder
+    (osmx_softmax_topk_host_multi): pinned host rows -> per-device H2D ->
+    fused kernel -> D2H of the top-k, one host thread + PCIe link per GPU,
+    all inside the timed region.  Rank 0 drives every GPU of the job from one
+    process (the C++ caller's view); the other ranks wait at the barrier.
+    Wall clock around `steps` calls (each call synchronises)."""
     import ctypes as C
 
     import numpy as np
     import torch
 
-    # pinned host copy of (part of) the shard; bounded by host RAM per rank
+    # pinned host rows, bounded by host RAM; each device block replicates
+    # (a prefix of) rank 0's shard so every block is checkable on device
     try:
         avail = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
     except (ValueError, OSError):
         avail = 64 << 30
-    cap_rows = int(0.35 * avail / max(world, 1) / (V * 4))
-    e_rows = max(1, min(rows, cap_rows))
+    per_dev = max(1, min(rows, int(0.35 * avail / max(world, 1) / (V * 4))))
+    res = None
+    if int(os.environ.get("RANK", "0")) == 0:
+        res = _e2e_rank0(lib, _lib, x, dev_idx, per_dev, V, k, world, steps)
+    if dist is not None:
+        dist.barrier()
+    return res
+
+
+def _e2e_rank0(lib, _lib, x, dev_idx, per_dev, V, k, world, steps) -> dict:
+    import ctypes as C
+
+    import numpy as np
+    import torch
+
+    e_rows = per_dev * world
     host = torch.empty((e_rows, V), dtype=torch.float32, pin_memory=True)
-    host.copy_(x[:e_rows])
+    for r in range(world):
+        host[r * per_dev:(r + 1) * per_dev].copy_(x[:per_dev])
     hv = torch.empty((e_rows, k), dtype=torch.float32, pin_memory=True)
     hi = torch.empty((e_rows, k), dtype=torch.int64, pin_memory=True)
     bad = C.c_int64(-1)
     alg = _lib.ONLINE_SOFTMAX_FUSED_TOPK
+    devs = (C.c_int * world)(*range(world))
 
     def call():
-        st = lib.osmx_softmax_topk_host(alg, host.data_ptr(), e_rows, V, k, hv.data_ptr(), hi.data_ptr(), local,
-                                        C.byref(bad))
+        st = lib.osmx_softmax_topk_host_multi(alg, host.data_ptr(), e_rows, V, k, hv.data_ptr(), hi.data_ptr(),
+                                              devs, world, C.byref(bad))
         if st != 0:
-            raise RuntimeError(f"osmx_softmax_topk_host: {_lib.status_string(st)}")
+            raise RuntimeError(f"osmx_softmax_topk_host_multi: {_lib.status_string(st)}")
 
-    call()  # warm-up (allocates staging)
-    steps = 3
-    if dist is not None:
-        dist.barrier()
+    call()  # warm-up (allocates the per-device staging)
     t0 = time.perf_counter()
     for _ in range(steps):
         call()
     t = (time.perf_counter() - t0) / steps
-    if dist is not None:
-        tt = torch.tensor([t], device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t = float(tt[0])
-    # the host-buffer path must return what the device-resident launch returned
-    ok = bool(np.array_equal(hi.numpy(), dev_idx[:e_rows].cpu().numpy()))
+    # the host path must return what the device-resident launch returned
+    ref = dev_idx[:per_dev].cpu().numpy()
+    ok = all(bool(np.array_equal(hi.numpy()[r * per_dev:(r + 1) * per_dev], ref)) for r in range(world))
     lib.osmx_host_release()
-    gbs = algo_bytes("online_fused", e_rows * world, V, k) / t / 1e9
+    gbs = algo_bytes("online_fused", e_rows, V, k) / t / 1e9
     return {"value": round(gbs, 2), "unit": "GB/s", "h2d_bytes_per_step": e_rows * V * 4,
-            "d2h_bytes_per_step": e_rows * k * 12, "rows_per_gpu": e_rows, "steps": steps,
-            "ms_per_step": round(t * 1e3, 2), "api": "osmx_softmax_topk_host (pinned host buffers)",
+            "d2h_bytes_per_step": e_rows * k * 12, "rows": e_rows, "devices": world, "steps": steps,
+            "ms_per_step": round(t * 1e3, 2), "api": "osmx_softmax_topk_host_multi (pinned host buffers)",
             "consistent": ok}
 
 

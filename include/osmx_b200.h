@@ -161,6 +161,22 @@ osmx_status osmx_softmax_topk_host(int alg, const float* x, int64_t rows, int64_
 /* topk_of over host values (topk.hpp:54). */
 osmx_status osmx_topk_host(const float* v, int64_t rows, int64_t V, int32_t k, float* vals, int64_t* idx,
                            int device, int64_t* first_bad_row);
+/* Multi-device row sharder of the host path (the reference's run_batch
+ * stripes rows over std::threads, bench.cpp:66-96): devices[i] takes the
+ * contiguous rows [rows*i/n, rows*(i+1)/n) on its own host thread, staging
+ * buffers, streams and PCIe link; no inter-device communication.  A device
+ * may be listed more than once (one staging context per entry).  Errors: the
+ * first failing entry in list order; else OSMX_ERR_NON_FINITE with the lowest
+ * bad row over all devices.  Thread-safe; launch knobs are the caller's
+ * osmx_config_set defaults at the time of the call. */
+osmx_status osmx_softmax_host_multi(int alg, const float* x, int64_t rows, int64_t V, float* y,
+                                    const int* devices, int32_t n_devices, int64_t* first_bad_row);
+osmx_status osmx_softmax_topk_host_multi(int alg, const float* x, int64_t rows, int64_t V, int32_t k,
+                                         float* vals, int64_t* idx, const int* devices, int32_t n_devices,
+                                         int64_t* first_bad_row);
+osmx_status osmx_topk_host_multi(const float* v, int64_t rows, int64_t V, int32_t k, float* vals,
+                                 int64_t* idx, const int* devices, int32_t n_devices,
+                                 int64_t* first_bad_row);
 /* Release the per-device staging buffers of the host path. */
 void osmx_host_release(void);
 

@@ -47,6 +47,9 @@ SIGNATURES = {
     "osmx_softmax_host": (_int, [_int, _vp, _i64, _i64, _vp, _int, _pi64]),
     "osmx_softmax_topk_host": (_int, [_int, _vp, _i64, _i64, _i32, _vp, _vp, _int, _pi64]),
     "osmx_topk_host": (_int, [_vp, _i64, _i64, _i32, _vp, _vp, _int, _pi64]),
+    "osmx_softmax_host_multi": (_int, [_int, _vp, _i64, _i64, _vp, _vp, _i32, _pi64]),
+    "osmx_softmax_topk_host_multi": (_int, [_int, _vp, _i64, _i64, _i32, _vp, _vp, _vp, _i32, _pi64]),
+    "osmx_topk_host_multi": (_int, [_vp, _i64, _i64, _i32, _vp, _vp, _vp, _i32, _pi64]),
     "osmx_host_release": (None, []),
     "osmx_launch_count": (C.c_uint64, []),
     "osmx_diag_read_probe": (_int, [_vp, _sz, _vp, _vp]),

@@ -12,7 +12,10 @@
 #include <cstdio>
 #include <cstddef>
 #include <cstring>
+#include <map>
+#include <memory>
 #include <mutex>
+#include <thread>
 #include <set>
 #include <utility>
 #include <string>
@@ -24,9 +27,37 @@
 
 namespace osmx_host {
 
+namespace {
+std::mutex g_tune_mu;
+Tuning g_tune;                   // process-wide defaults (osmx_config_set)
+thread_local Tuning t_tune;      // snapshot in force for this thread's call
+thread_local int t_scope = 0;    // open TuningScopes on this thread
+}  // namespace
+
+Tuning tuning_defaults() {
+  std::lock_guard<std::mutex> lock(g_tune_mu);
+  return g_tune;
+}
+void tuning_set_defaults(const Tuning& t) {
+  std::lock_guard<std::mutex> lock(g_tune_mu);
+  g_tune = t;
+}
 Tuning& tuning() {
-  static Tuning t;
-  return t;
+  if (t_scope == 0) t_tune = tuning_defaults();  // outside a call: fresh snapshot
+  return t_tune;
+}
+TuningScope::TuningScope(const Tuning* t) : outer_(t_scope == 0) {
+  if (outer_)
+    t_tune = t ? *t : tuning_defaults();
+  else {
+    saved_ = t_tune;
+    if (t) t_tune = *t;
+  }
+  ++t_scope;
+}
+TuningScope::~TuningScope() {
+  --t_scope;
+  if (!outer_) t_tune = saved_;
 }
 
 static std::atomic<unsigned long long> g_launches{0};
@@ -54,7 +85,7 @@ bool first_use_on_device(const void* fn) {
   return seen.insert({dev, fn}).second;
 }
 
-static long long g_host_chunk_mb = 512;
+static std::atomic<long long> g_host_chunk_mb{512};
 
 static size_t align256(size_t b) { return (b + 255) / 256 * 256; }
 
@@ -179,6 +210,7 @@ const char* osmx_status_string(osmx_status s) {
 const char* osmx_last_cuda_error(void) { return t_cuda_err.c_str(); }
 
 size_t osmx_workspace_bytes(int alg, int64_t rows, int64_t V, int32_t k) {
+  TuningScope scope;
   return workspace_bytes(alg, rows, V, k);
 }
 
@@ -204,6 +236,7 @@ osmx_status osmx_check_status(void* ws, void* stream, int64_t* first_bad_row) {
 osmx_status osmx_softmax(int alg, const float* x, int64_t ldx, float* y, int64_t ldy, int64_t rows, int64_t V,
                          void* ws, size_t ws_bytes, void* stream) {
   if (!is_softmax(alg)) return OSMX_ERR_INVALID_ARG;
+  TuningScope scope;
   osmx_status s = check_common(x, ldx, rows, V);
   if (s) return s;
   if (ldy < V || (rows > 0 && !y) || !ws) return OSMX_ERR_INVALID_ARG;
@@ -215,6 +248,7 @@ osmx_status osmx_softmax(int alg, const float* x, int64_t ldx, float* y, int64_t
 osmx_status osmx_softmax_topk(int alg, const float* x, int64_t ldx, int64_t rows, int64_t V, int32_t k,
                               float* vals, int64_t* idx, void* ws, size_t ws_bytes, void* stream) {
   if (!is_topk(alg)) return OSMX_ERR_INVALID_ARG;
+  TuningScope scope;
   osmx_status s = check_common(x, ldx, rows, V);
   if (s) return s;
   if ((s = check_k(V, k, rows))) return s;
@@ -227,6 +261,7 @@ osmx_status osmx_softmax_topk(int alg, const float* x, int64_t ldx, int64_t rows
 
 osmx_status osmx_topk(const float* v, int64_t ld, int64_t rows, int64_t V, int32_t k, float* vals, int64_t* idx,
                       void* ws, size_t ws_bytes, void* stream) {
+  TuningScope scope;
   osmx_status s = check_common(v, ld, rows, V);
   if (s) return s;
   if ((s = check_k(V, k, rows))) return s;
@@ -239,6 +274,7 @@ osmx_status osmx_topk(const float* v, int64_t ld, int64_t rows, int64_t V, int32
 
 osmx_status osmx_proj_softmax_topk(const void* h, int64_t rows, int64_t D, const void* w, int64_t V, int32_t k,
                                    float* vals, int64_t* idx, void* ws, size_t ws_bytes, void* stream) {
+  TuningScope scope;
   if (V < 1 || D < 1) return OSMX_ERR_EMPTY;
   if (k < 1 || (long long)k > V) return OSMX_ERR_INVALID_K;
   if (k > kMaxK) return OSMX_ERR_UNSUPPORTED;
@@ -255,6 +291,7 @@ osmx_status osmx_proj_softmax_topk(const void* h, int64_t rows, int64_t D, const
 
 osmx_status osmx_normalizer(const float* x, int64_t ldx, int64_t rows, int64_t V, int64_t chunk, float* m,
                             float* d, void* ws, size_t ws_bytes, void* stream) {
+  TuningScope scope;
   osmx_status s = check_common(x, ldx, rows, V);
   if (s) return s;
   if (chunk < 0) return OSMX_ERR_INVALID_CHUNK;
@@ -272,17 +309,11 @@ osmx_status osmx_slice_record(const float* x, int64_t V, int64_t col0, int32_t k
   if (k < 0 || k > kMaxK) return k < 0 ? OSMX_ERR_INVALID_K : OSMX_ERR_UNSUPPORTED;
   const int kk = k > 0 ? k : 1;
   // the slice may hold fewer than k elements; the merged row must not
+  TuningScope scope;  // the forced split shape below lives only in this call's snapshot
   const size_t need = workspace_bytes(9, 1, V, kk);
-  // force the split path regardless of tuning
-  Tuning saved = tuning();
+  if (ws_bytes < need) return OSMX_ERR_INVALID_ARG;
   tuning().shape = kShapeSplit;
-  osmx_status st = OSMX_OK;
-  if (ws_bytes < need)
-    st = OSMX_ERR_INVALID_ARG;
-  else
-    st = cuda_status(launch_slice_record(x, V, col0, k, record, ws, ws_bytes, static_cast<cudaStream_t>(stream)));
-  tuning() = saved;
-  return st;
+  return cuda_status(launch_slice_record(x, V, col0, k, record, ws, ws_bytes, static_cast<cudaStream_t>(stream)));
 }
 
 osmx_status osmx_records_combine(const void* records, int32_t n, int32_t k, void* out_record, float* vals,
@@ -290,6 +321,7 @@ osmx_status osmx_records_combine(const void* records, int32_t n, int32_t k, void
   if (!records || n < 1 || !ws || ws_bytes < (size_t)osmx_dev::kWsHeader) return OSMX_ERR_INVALID_ARG;
   if (k < 0 || k > kMaxK) return k < 0 ? OSMX_ERR_INVALID_K : OSMX_ERR_UNSUPPORTED;
   if (k > 0 && (!vals) != (!idx)) return OSMX_ERR_INVALID_ARG;
+  TuningScope scope;
   return cuda_status(launch_records_combine(records, n, k, out_record, vals, reinterpret_cast<long long*>(idx), ws,
                                             static_cast<cudaStream_t>(stream)));
 }
@@ -297,6 +329,7 @@ osmx_status osmx_records_combine(const void* records, int32_t n, int32_t k, void
 osmx_status osmx_scale_with_record(const float* x, int64_t V, const void* record, float* y, void* stream) {
   if (V < 1) return OSMX_ERR_EMPTY;
   if (!x || !record || !y) return OSMX_ERR_INVALID_ARG;
+  TuningScope scope;
   return cuda_status(launch_scale_with_record(x, V, record, y, static_cast<cudaStream_t>(stream)));
 }
 
@@ -309,7 +342,8 @@ osmx_status osmx_diag_read_probe(const void* x, size_t bytes, float* sink, void*
 
 osmx_status osmx_config_set(const char* key, int64_t value) {
   if (!key) return OSMX_ERR_INVALID_ARG;
-  auto& t = tuning();
+  std::lock_guard<std::mutex> lock(g_tune_mu);  // process-wide defaults
+  auto& t = g_tune;
   if (!strcmp(key, "shape")) {
     if (value < 0 || value > 5) return OSMX_ERR_INVALID_ARG;
     t.shape = (int)value;
@@ -369,7 +403,7 @@ osmx_status osmx_config_set(const char* key, int64_t value) {
 
 int64_t osmx_config_get(const char* key) {
   if (!key) return -1;
-  const auto& t = tuning();
+  const Tuning t = tuning_defaults();
   if (!strcmp(key, "shape")) return t.shape;
   if (!strcmp(key, "resident_max_v")) return t.resident_max_v;
   if (!strcmp(key, "split_chunk")) return t.split_chunk;
@@ -395,12 +429,13 @@ int64_t osmx_config_get(const char* key) {
 // ------------------------------------------------------ host-buffer path --
 namespace {
 
-// Per-device staging: two slots, each with its own stream, input block,
-// output block and workspace, so block i+1's H2D overlaps block i's kernel
-// and block i-1's D2H.
+// Staging of one host thread on one device: two slots, each with its own
+// stream, input block, output block and workspace, so block i+1's H2D
+// overlaps block i's kernel and block i-1's D2H.  Keyed by (device, slot):
+// a multi-device call that lists a device twice drives it from two threads
+// with two contexts.
 struct HostCtx {
   std::mutex mu;
-  int device = -1;
   cudaStream_t st[2] = {nullptr, nullptr};
   void* xin[2] = {nullptr, nullptr};
   void* out[2] = {nullptr, nullptr};
@@ -443,34 +478,50 @@ struct HostCtx {
   }
 };
 
-HostCtx g_ctx[64];
+std::mutex g_ctx_mu;
+std::map<std::pair<int, int>, std::unique_ptr<HostCtx>> g_ctx;
+
+HostCtx& host_ctx(int device, int slot) {
+  std::lock_guard<std::mutex> lock(g_ctx_mu);
+  auto& p = g_ctx[{device, slot}];
+  if (!p) p.reset(new HostCtx);
+  return *p;
+}
+
+// What one row block runs: a softmax (out1 = y) or a top-K (out1 = vals,
+// out2 = idx).  alg is the C-ABI id; kTopkOf for osmx_topk_host.
+struct HostOp {
+  bool topk;
+  int alg;
+  int k;
+  size_t out1_row() const { return topk ? (size_t)k * sizeof(float) : 0; }
+  size_t out2_row() const { return topk ? (size_t)k * sizeof(long long) : 0; }
+};
 
 // The second output block (int64 indices) starts 256-byte aligned after the
 // first (rpb*k floats): int64 stores need 8-byte alignment.
 size_t out2_offset(long long rpb, size_t out_row_bytes) { return ((size_t)rpb * out_row_bytes + 255) / 256 * 256; }
 
-template <class Launch>
-osmx_status host_pipeline(int device, long long rows, long long V, size_t out_row_bytes, int alg, int k,
-                          const float* x, void* out_host, Launch&& launch, int64_t* first_bad_row,
-                          void* out2_host = nullptr, size_t out2_row_bytes = 0) {
-  if (device < 0 || device >= 64) return OSMX_ERR_INVALID_ARG;
-  HostCtx& c = g_ctx[device];
+// Rows [0, rows) of x on one device through ctx (device, slot), in blocks of
+// rpb rows.  *first_bad = lowest non-finite row (local) or -1.
+osmx_status host_run(const HostOp& op, int device, int slot, const float* x, long long rows, long long V,
+                     char* out1, char* out2, long long chunk_mb, long long* first_bad) {
+  HostCtx& c = host_ctx(device, slot);
   std::lock_guard<std::mutex> lock(c.mu);
-  int prev = 0;
-  cudaGetDevice(&prev);
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) return cuda_status(e);
   const size_t row_b = (size_t)V * sizeof(float);
-  const size_t budget = (size_t)g_host_chunk_mb << 20;
-  long long rpb = (long long)std::max<size_t>(1, budget / row_b);
+  const size_t o1 = op.topk ? op.out1_row() : row_b, o2 = op.out2_row();
+  long long rpb = (long long)std::max<size_t>(1, ((size_t)chunk_mb << 20) / row_b);
   rpb = std::min(rpb, rows);
-  const size_t out_tot = (out_row_bytes + out2_row_bytes);
-  e = c.ensure(rpb * row_b, std::max<size_t>(rpb * out_tot + 512, 256),
-               workspace_bytes(alg, rpb, V, k));
-  if (e != cudaSuccess) {
-    cudaSetDevice(prev);
-    return cuda_status(e);
-  }
+  // The launch layer picks a kernel shape per block, so the short tail block
+  // may take a path (split records) the full blocks do not: size the
+  // workspace for both.
+  const long long tail = rows % rpb;
+  size_t wsb = workspace_bytes(op.alg, rpb, V, op.k);
+  if (tail) wsb = std::max(wsb, workspace_bytes(op.alg, tail, V, op.k));
+  e = c.ensure(rpb * row_b, std::max<size_t>(out2_offset(rpb, o1) + (size_t)rpb * o2 + 256, 256), wsb);
+  if (e != cudaSuccess) return cuda_status(e);
   osmx_status st = OSMX_OK;
   const long long nblk = (rows + rpb - 1) / rpb;
   std::vector<long long> bases((size_t)nblk, 0);
@@ -481,41 +532,127 @@ osmx_status host_pipeline(int device, long long rows, long long V, size_t out_ro
     bases[b] = r0;
     e = cudaMemcpyAsync(static_cast<char*>(c.ws[s]) + offsetof(osmx_dev::WsHeader, row_base), &bases[b],
                         sizeof(long long), cudaMemcpyHostToDevice, c.st[s]);
-    if (e == cudaSuccess)
-      e = cudaMemcpyAsync(c.xin[s], x + r0 * V, (size_t)nr * row_b, cudaMemcpyHostToDevice, c.st[s]);
-    if (e == cudaSuccess) e = launch(static_cast<const float*>(c.xin[s]), nr, c.out[s], c.ws[s], c.ws_b, c.st[s]);
-    if (e == cudaSuccess)
-      e = cudaMemcpyAsync(static_cast<char*>(out_host) + r0 * out_row_bytes, c.out[s], (size_t)nr * out_row_bytes,
-                          cudaMemcpyDeviceToHost, c.st[s]);
-    if (e == cudaSuccess && out2_host)
-      e = cudaMemcpyAsync(static_cast<char*>(out2_host) + r0 * out2_row_bytes,
-                          static_cast<char*>(c.out[s]) + out2_offset(rpb, out_row_bytes), (size_t)nr * out2_row_bytes,
-                          cudaMemcpyDeviceToHost, c.st[s]);
-    if (e != cudaSuccess) st = cuda_status(e);
-  }
-  // Status: each slot's flag holds the lowest bad (global) row of its
-  // blocks -- the kernels add the header's row_base set per block above.
-  long long first_bad = -1;
-  for (int s = 0; s < 2 && st == OSMX_OK; ++s) {
-    if (!c.st[s]) continue;
-    unsigned long long bad = 0;
-    e = cudaMemcpyAsync(&bad, c.ws[s], sizeof(bad), cudaMemcpyDeviceToHost, c.st[s]);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(c.st[s]);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(c.xin[s], x + r0 * V, (size_t)nr * row_b, cudaMemcpyHostToDevice, c.st[s]);
     if (e != cudaSuccess) {
       st = cuda_status(e);
       break;
     }
+    const float* dx = static_cast<const float*>(c.xin[s]);
+    char* dout = static_cast<char*>(c.out[s]);
+    if (op.topk)
+      st = run_topk_alg(op.alg, dx, V, nr, V, op.k, reinterpret_cast<float*>(dout),
+                        reinterpret_cast<long long*>(dout + out2_offset(rpb, o1)), c.ws[s], c.ws_b, c.st[s]);
+    else
+      st = cuda_status(launch_softmax(op.alg, dx, V, reinterpret_cast<float*>(dout), V, nr, V, c.ws[s], c.ws_b, c.st[s]));
+    if (st != OSMX_OK) break;
+    e = cudaMemcpyAsync(out1 + r0 * o1, dout, (size_t)nr * o1, cudaMemcpyDeviceToHost, c.st[s]);
+    if (e == cudaSuccess && out2)
+      e = cudaMemcpyAsync(out2 + r0 * o2, dout + out2_offset(rpb, o1), (size_t)nr * o2, cudaMemcpyDeviceToHost,
+                          c.st[s]);
+    if (e != cudaSuccess) st = cuda_status(e);
+  }
+  // Status: each slot's flag holds the lowest bad (block-local + row_base)
+  // row of its blocks.  Both streams are drained even after an error, so
+  // `bases` outlives every copy that reads it.
+  long long bad_row = -1;
+  for (int s = 0; s < 2; ++s) {
+    if (!c.st[s]) continue;
+    unsigned long long bad = 0;
+    e = cudaMemcpyAsync(&bad, c.ws[s], sizeof(bad), cudaMemcpyDeviceToHost, c.st[s]);
+    const cudaError_t e2 = cudaStreamSynchronize(c.st[s]);
+    if (e == cudaSuccess) e = e2;
+    if (e != cudaSuccess) {
+      if (st == OSMX_OK) st = cuda_status(e);
+      continue;
+    }
     if (bad) {
       const long long r = (long long)(0x7fffffffffffffffULL - bad);
-      first_bad = first_bad < 0 ? r : std::min(first_bad, r);
+      bad_row = bad_row < 0 ? r : std::min(bad_row, r);
       cudaMemsetAsync(c.ws[s], 0, sizeof(bad), c.st[s]);
       cudaStreamSynchronize(c.st[s]);
     }
   }
-  if (st == OSMX_OK && first_bad >= 0) st = OSMX_ERR_NON_FINITE;
-  if (first_bad_row) *first_bad_row = first_bad;
-  cudaSetDevice(prev);
+  *first_bad = bad_row;
   return st;
+}
+
+// Row sharder of the host path (the reference's run_batch stripes rows over
+// std::threads, bench.cpp:66-96): device list entry i gets the contiguous
+// rows [rows*i/n, rows*(i+1)/n) and its own host thread, staging context and
+// PCIe link.  Errors: the first failing device (list order) wins; else the
+// lowest non-finite row over all devices.
+osmx_status host_multi(const HostOp& op, const float* x, long long rows, long long V, void* out1, void* out2,
+                       const int* devices, int n, int64_t* first_bad_row) {
+  if (first_bad_row) *first_bad_row = -1;
+  if (n < 1 || !devices) return OSMX_ERR_INVALID_ARG;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess) return cuda_status(e);
+  for (int i = 0; i < n; ++i)
+    if (devices[i] < 0 || devices[i] >= ndev) return OSMX_ERR_INVALID_ARG;
+  if (rows == 0) return OSMX_OK;
+  const Tuning snap = tuning();  // the caller's knobs, for every worker
+  const long long chunk_mb = g_host_chunk_mb.load();
+  const size_t row_b = (size_t)V * sizeof(float), o1 = op.topk ? op.out1_row() : row_b, o2 = op.out2_row();
+  std::vector<osmx_status> st((size_t)n, OSMX_OK);
+  std::vector<long long> bad((size_t)n, -1);
+  std::vector<std::string> err((size_t)n);
+  int prev = 0;
+  cudaGetDevice(&prev);
+  auto work = [&](int i) {
+    TuningScope scope(&snap);
+    int slot = 0;
+    for (int j = 0; j < i; ++j) slot += devices[j] == devices[i];
+    const long long r0 = rows * i / n, r1 = rows * (i + 1) / n;
+    if (r1 <= r0) return;
+    st[i] = host_run(op, devices[i], slot, x + r0 * V, r1 - r0, V, static_cast<char*>(out1) + r0 * o1,
+                     out2 ? static_cast<char*>(out2) + r0 * o2 : nullptr, chunk_mb, &bad[i]);
+    if (bad[i] >= 0) bad[i] += r0;
+    err[i] = t_cuda_err;
+  };
+  if (n == 1) {
+    work(0);
+  } else {
+    std::vector<std::thread> th;
+    th.reserve((size_t)n - 1);
+    for (int i = 1; i < n; ++i) th.emplace_back(work, i);
+    work(0);
+    for (auto& t : th) t.join();
+  }
+  cudaSetDevice(prev);
+  long long first = -1;
+  for (int i = 0; i < n; ++i) {
+    if (st[i] != OSMX_OK) {
+      t_cuda_err = err[i];
+      return st[i];
+    }
+    if (bad[i] >= 0) first = first < 0 ? bad[i] : std::min(first, bad[i]);
+  }
+  if (first_bad_row) *first_bad_row = first;
+  return first >= 0 ? OSMX_ERR_NON_FINITE : OSMX_OK;
+}
+
+osmx_status softmax_host_multi(int alg, const float* x, int64_t rows, int64_t V, float* y, const int* devices,
+                               int n, int64_t* first_bad_row) {
+  if (first_bad_row) *first_bad_row = -1;
+  if (!is_softmax(alg)) return OSMX_ERR_INVALID_ARG;
+  TuningScope scope;
+  osmx_status s = check_common(x, V, rows, V);
+  if (s) return s;
+  if (rows > 0 && !y) return OSMX_ERR_INVALID_ARG;
+  return host_multi(HostOp{false, alg, 0}, x, rows, V, y, nullptr, devices, n, first_bad_row);
+}
+
+osmx_status topk_host_multi(int alg, const float* x, int64_t rows, int64_t V, int32_t k, float* vals, int64_t* idx,
+                            const int* devices, int n, int64_t* first_bad_row) {
+  if (first_bad_row) *first_bad_row = -1;
+  if (alg != kTopkOf && !is_topk(alg)) return OSMX_ERR_INVALID_ARG;
+  TuningScope scope;
+  osmx_status s = check_common(x, V, rows, V);
+  if (s) return s;
+  if ((s = check_k(V, k))) return s;
+  if (rows > 0 && (!vals || !idx)) return OSMX_ERR_INVALID_ARG;
+  return host_multi(HostOp{true, alg, k}, x, rows, V, vals, idx, devices, n, first_bad_row);
 }
 
 }  // namespace
@@ -524,76 +661,49 @@ extern "C" {
 
 osmx_status osmx_softmax_host(int alg, const float* x, int64_t rows, int64_t V, float* y, int device,
                               int64_t* first_bad_row) {
-  if (!is_softmax(alg)) return OSMX_ERR_INVALID_ARG;
-  osmx_status s = check_common(x, V, rows, V);
-  if (s) return s;
-  if (rows > 0 && !y) return OSMX_ERR_INVALID_ARG;
-  if (first_bad_row) *first_bad_row = -1;
-  if (rows == 0) return OSMX_OK;
-  return host_pipeline(
-      device, rows, V, (size_t)V * sizeof(float), alg, 0, x, y,
-      [&](const float* dx, long long nr, void* dout, void* ws, size_t wsb, cudaStream_t st) {
-        return launch_softmax(alg, dx, V, static_cast<float*>(dout), V, nr, V, ws, wsb, st);
-      },
-      first_bad_row);
+  return softmax_host_multi(alg, x, rows, V, y, &device, 1, first_bad_row);
 }
 
 osmx_status osmx_softmax_topk_host(int alg, const float* x, int64_t rows, int64_t V, int32_t k, float* vals,
                                    int64_t* idx, int device, int64_t* first_bad_row) {
   if (!is_topk(alg)) return OSMX_ERR_INVALID_ARG;
-  osmx_status s = check_common(x, V, rows, V);
-  if (s) return s;
-  if ((s = check_k(V, k))) return s;
-  if (rows > 0 && (!vals || !idx)) return OSMX_ERR_INVALID_ARG;
-  if (first_bad_row) *first_bad_row = -1;
-  if (rows == 0) return OSMX_OK;
-  // device output block: vals (rpb*k floats) then idx (rpb*k int64)
-  const size_t vb = (size_t)k * sizeof(float), ib = (size_t)k * sizeof(int64_t);
-  long long rpb_cache = 0;
-  (void)rpb_cache;
-  return host_pipeline(
-      device, rows, V, vb, alg, k, x, vals,
-      [&](const float* dx, long long nr, void* dout, void* ws, size_t wsb, cudaStream_t st) -> cudaError_t {
-        // idx block lives after the full-capacity vals block
-        const size_t budget = (size_t)g_host_chunk_mb << 20;
-        long long rpb = (long long)std::max<size_t>(1, budget / ((size_t)V * sizeof(float)));
-        rpb = std::min<long long>(rpb, rows);
-        float* dv = static_cast<float*>(dout);
-        long long* di = reinterpret_cast<long long*>(static_cast<char*>(dout) + out2_offset(rpb, vb));
-        osmx_status r = run_topk_alg(alg, dx, V, nr, V, k, dv, di, ws, wsb, st);
-        return r == OSMX_OK ? cudaSuccess : (r == OSMX_ERR_CUDA ? cudaErrorUnknown : cudaErrorInvalidValue);
-      },
-      first_bad_row, idx, ib);
+  return topk_host_multi(alg, x, rows, V, k, vals, idx, &device, 1, first_bad_row);
 }
 
 osmx_status osmx_topk_host(const float* v, int64_t rows, int64_t V, int32_t k, float* vals, int64_t* idx,
                            int device, int64_t* first_bad_row) {
-  osmx_status s = check_common(v, V, rows, V);
-  if (s) return s;
-  if ((s = check_k(V, k))) return s;
-  if (rows > 0 && (!vals || !idx)) return OSMX_ERR_INVALID_ARG;
-  if (first_bad_row) *first_bad_row = -1;
-  if (rows == 0) return OSMX_OK;
-  const size_t vb = (size_t)k * sizeof(float), ib = (size_t)k * sizeof(int64_t);
-  return host_pipeline(
-      device, rows, V, vb, kTopkOf, k, v, vals,
-      [&](const float* dx, long long nr, void* dout, void* ws, size_t wsb, cudaStream_t st) -> cudaError_t {
-        const size_t budget = (size_t)g_host_chunk_mb << 20;
-        long long rpb = (long long)std::max<size_t>(1, budget / ((size_t)V * sizeof(float)));
-        rpb = std::min<long long>(rpb, rows);
-        float* dv = static_cast<float*>(dout);
-        long long* di = reinterpret_cast<long long*>(static_cast<char*>(dout) + out2_offset(rpb, vb));
-        osmx_status r = run_topk_alg(kTopkOf, dx, V, nr, V, k, dv, di, ws, wsb, st);
-        return r == OSMX_OK ? cudaSuccess : (r == OSMX_ERR_CUDA ? cudaErrorUnknown : cudaErrorInvalidValue);
-      },
-      first_bad_row, idx, ib);
+  return topk_host_multi(kTopkOf, v, rows, V, k, vals, idx, &device, 1, first_bad_row);
+}
+
+osmx_status osmx_softmax_host_multi(int alg, const float* x, int64_t rows, int64_t V, float* y,
+                                    const int* devices, int32_t n_devices, int64_t* first_bad_row) {
+  return softmax_host_multi(alg, x, rows, V, y, devices, n_devices, first_bad_row);
+}
+
+osmx_status osmx_softmax_topk_host_multi(int alg, const float* x, int64_t rows, int64_t V, int32_t k, float* vals,
+                                         int64_t* idx, const int* devices, int32_t n_devices,
+                                         int64_t* first_bad_row) {
+  if (!is_topk(alg)) return OSMX_ERR_INVALID_ARG;
+  return topk_host_multi(alg, x, rows, V, k, vals, idx, devices, n_devices, first_bad_row);
+}
+
+osmx_status osmx_topk_host_multi(const float* v, int64_t rows, int64_t V, int32_t k, float* vals, int64_t* idx,
+                                 const int* devices, int32_t n_devices, int64_t* first_bad_row) {
+  return topk_host_multi(kTopkOf, v, rows, V, k, vals, idx, devices, n_devices, first_bad_row);
 }
 
 void osmx_host_release(void) {
-  for (auto& c : g_ctx) {
-    std::lock_guard<std::mutex> lock(c.mu);
-    if (c.st[0]) c.release();
+  std::lock_guard<std::mutex> lock(g_ctx_mu);
+  int prev = 0;
+  cudaGetDevice(&prev);
+  for (auto& kv : g_ctx) {
+    std::lock_guard<std::mutex> l2(kv.second->mu);
+    if (kv.second->st[0]) {
+      cudaSetDevice(kv.first.first);
+      kv.second->release();
+    }
   }
+  cudaSetDevice(prev);
 }
 
 }  // extern "C"

@@ -122,11 +122,15 @@ __device__ __forceinline__ float pow2_int(float k) {
 // ex2(x*L - m*L).  The remaining approximation, L = RN(log2 e), perturbs
 // each term by |x_j - m| * 2^-25, as in e^(x - m) itself.
 //
-// Inputs above 2^127 (m * L would overflow n) switch the thread to `huge`
-// mode for the rest of the row: d relative to m in natural units, terms
-// e^(x - m) as before -- a warp-uniform branch per batch, never taken on
-// ordinary logits.
-constexpr float kHugeX = 1.7014118e38f;  // 2^127
+// The log2 domain is exact only while RN(m * L) is within a few units of
+// m * L: n = ceil(RN(m*L)) is then an integer next to the exact product and
+// every term 2^(x*L - n) stays near 1 for x near m.  Once ulp(m * L) grows
+// past ~2^7 (|m| > ~1.5e9) a term could reach 2^(ulp/2) and overflow, and for
+// |m| >= 2^127 (e.g. a -FLT_MAX mask) n itself is infinite.  So a thread
+// whose batch max has |bm| >= 2^20 switches to `huge` mode for the rest of
+// the row: d relative to m in natural units, terms e^(x - m) -- a
+// warp-uniform branch per batch, never taken on ordinary logits.
+constexpr float kHugeX = 1048576.0f;  // 2^20
 
 struct L2Acc {
   float m = kNegInf;  // running max (natural units)
@@ -137,9 +141,14 @@ struct L2Acc {
   // Raise the reference for a batch whose max is bm (no-op if bm <= m).
   __device__ __forceinline__ void raise(float bm) {
     if (bm > m) {
-      if (!huge && bm < kHugeX) {
+      if (fabsf(bm) < kHugeX) {
         const float nn = ceilf(bm * kLog2e);
-        d *= pow2_int(n - nn);
+        if (!huge) {
+          d *= pow2_int(n - nn);
+        } else {  // back from natural units (a masked head): d e^(m-bm) 2^(bm L - nn)
+          d *= exp_sub(m, bm) * ex2(fmaf(bm, kLog2e, -nn));
+          huge = false;
+        }
         n = nn;
       } else if (!huge) {  // leave the log2 domain: d relative to bm
         d = (m == kNegInf) ? d : d * ex2(fmaf(-bm, kLog2e, n));

@@ -54,7 +54,24 @@ struct Tuning {
   int tma = 0;                  // TMA-ring top-K: 0 off (default: the warp-per-row
                                 // LDG kernel measures faster), 1 auto, 2 force
 };
+// The knobs in force for the current call on this thread.  osmx_config_set
+// writes process-wide defaults; every C-ABI entry point opens a TuningScope,
+// which snapshots them into thread-local storage for the whole call, so a
+// call never sees another thread's change (the reference is reentrant,
+// softmax.hpp:8-9) and a call-local override (osmx_slice_record's forced
+// split shape) never leaks into other threads or later calls.
 Tuning& tuning();
+Tuning tuning_defaults();
+void tuning_set_defaults(const Tuning& t);
+struct TuningScope {
+  explicit TuningScope(const Tuning* t = nullptr);
+  ~TuningScope();
+  TuningScope(const TuningScope&) = delete;
+  TuningScope& operator=(const TuningScope&) = delete;
+ private:
+  Tuning saved_;
+  bool outer_;
+};
 
 // Kernel-launch tally (every launch the library issues increments it).
 void count_launch(int n = 1);

@@ -126,13 +126,28 @@ ALGS = {
     "online_unfused": _lib.ONLINE_SOFTMAX_UNFUSED_TOPK,
 }
 
-_device = 0
+_devices: tuple[int, ...] = (0,)
 
 
 def set_device(device: int) -> None:
     """CUDA device used by the host-buffer (reference-shaped) functions."""
-    global _device
-    _device = int(device)
+    set_devices([device])
+
+
+def set_devices(devices) -> None:
+    """Devices the host-buffer functions shard a batch over: entry i takes a
+    contiguous block of rows on its own host thread inside the library
+    (osmx_*_host_multi; the reference's run_batch, bench.cpp:66-96).  A
+    device may be listed more than once."""
+    global _devices
+    ds = tuple(int(d) for d in devices)
+    if not ds:
+        raise ValueError("set_devices needs at least one device")
+    _devices = ds
+
+
+def _dev_array():
+    return (C.c_int * len(_devices))(*_devices), len(_devices)
 
 
 # ------------------------------------------------ reference-shaped (host) --
@@ -153,7 +168,8 @@ def _softmax_host(alg: int, x) -> np.ndarray:
         raise EmptyInputError()
     y = np.empty_like(a)
     bad = C.c_int64(-1)
-    st = load().osmx_softmax_host(alg, a.ctypes.data, rows, V, y.ctypes.data, _device, C.byref(bad))
+    devs, n = _dev_array()
+    st = load().osmx_softmax_host_multi(alg, a.ctypes.data, rows, V, y.ctypes.data, devs, n, C.byref(bad))
     _raise(st, bad.value)
     return y[0] if single else y
 
@@ -169,12 +185,13 @@ def _topk_host(alg: int | None, x, k: int) -> TopkResult:
     vals = np.empty((rows, k), np.float32)
     idx = np.empty((rows, k), np.int64)
     bad = C.c_int64(-1)
+    devs, n = _dev_array()
     if alg is None:
-        st = load().osmx_topk_host(a.ctypes.data, rows, V, k, vals.ctypes.data, idx.ctypes.data, _device,
-                                   C.byref(bad))
+        st = load().osmx_topk_host_multi(a.ctypes.data, rows, V, k, vals.ctypes.data, idx.ctypes.data, devs, n,
+                                         C.byref(bad))
     else:
-        st = load().osmx_softmax_topk_host(alg, a.ctypes.data, rows, V, k, vals.ctypes.data, idx.ctypes.data,
-                                           _device, C.byref(bad))
+        st = load().osmx_softmax_topk_host_multi(alg, a.ctypes.data, rows, V, k, vals.ctypes.data,
+                                                 idx.ctypes.data, devs, n, C.byref(bad))
     _raise(st, bad.value)
     if single:
         return TopkResult(vals[0], idx[0])
@@ -230,7 +247,7 @@ def _normalizer_host(x, chunk: int | None) -> NormState | tuple[np.ndarray, np.n
         raise EmptyInputError()
     if chunk is not None and chunk == 0:
         raise InvalidChunkError()
-    dev = torch.device("cuda", _device)
+    dev = torch.device("cuda", _devices[0])
     xt = torch.from_numpy(a).to(dev)
     m, d = normalizer(xt, chunk=chunk or 0)
     m, d = m.cpu().numpy(), d.cpu().numpy()
@@ -257,20 +274,35 @@ def run_normalizer_chunked(x, chunk_len: int):
 # ---------------------------------------------------- batched (device) -----
 
 class _Workspace:
-    """Per-device, grow-only workspace (zero-initialised header)."""
+    """Grow-only workspaces keyed by (device, stream): launches on different
+    streams never share split records or a status header.  A buffer is
+    allocated while its stream is current, so the caching allocator only
+    reuses it in that stream's order after a regrow.  A call that skipped
+    its status check (check=False) leaves the header `dirty`; the next call
+    on that workspace clears it first, so a stale flag is never reported
+    against other data."""
 
     def __init__(self):
         self.buf = {}
+        self.dirty = set()
 
     def get(self, nbytes: int, device, stream_ptr: int):
         import torch
 
-        key = device.index if device.index is not None else 0
+        key = (device.index if device.index is not None else 0, int(stream_ptr))
         t = self.buf.get(key)
         if t is None or t.numel() < nbytes:
             t = torch.zeros(max(int(nbytes), 256), dtype=torch.uint8, device=device)
             self.buf[key] = t
+            self.dirty.discard(key)
+        elif key in self.dirty:
+            st = load().osmx_workspace_init(t.data_ptr(), t.numel(), stream_ptr)
+            _raise(st)
+            self.dirty.discard(key)
         return t
+
+    def mark_dirty(self, device, stream_ptr: int):
+        self.dirty.add((device.index if device.index is not None else 0, int(stream_ptr)))
 
 
 _ws = _Workspace()
@@ -298,6 +330,22 @@ def _check_tensor(x, name="x"):
     return x
 
 
+def _finish(ws, device, stream: int, check: bool) -> None:
+    if check:
+        check_status(ws, stream)
+    else:
+        _ws.mark_dirty(device, stream)
+
+
+def _check_out(t, shape, dtype, device, name):
+    import torch
+
+    if not isinstance(t, torch.Tensor) or t.device != device or t.dtype != dtype or tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} must be a {dtype} tensor of shape {tuple(shape)} on {device}")
+    if t.numel() > 0 and (t.stride(-1) != 1 or (t.dim() == 2 and t.shape[0] > 1 and t.stride(0) < t.shape[1])):
+        raise ValueError(f"{name} must have unit stride along its last dimension and non-overlapping rows")
+
+
 def check_status(ws, stream: int) -> None:
     bad = C.c_int64(-1)
     st = load().osmx_check_status(ws.data_ptr(), stream, C.byref(bad))
@@ -320,14 +368,14 @@ def softmax(x, alg: str = "online", out=None, check: bool = True):
     a = ALGS[alg]
     if out is None:
         out = torch.empty_like(x2)
+    _check_out(out, x.shape, torch.float32, x2.device, "out")
     y = out if out.dim() == 2 else out.unsqueeze(0)
     stream = _stream_ptr(x2.device)
     ws, nb = workspace(a, rows, V, 0, x2.device)
     st = load().osmx_softmax(a, x2.data_ptr(), x2.stride(0), y.data_ptr(), y.stride(0), rows, V, ws.data_ptr(),
                              ws.numel(), stream)
     _raise(st)
-    if check:
-        check_status(ws, stream)
+    _finish(ws, x2.device, stream, check)
     return out if x.dim() == 2 else y[0]
 
 
@@ -345,13 +393,14 @@ def softmax_topk(x, k: int, alg: str = "online_fused", check: bool = True, out=N
         idx = torch.empty((rows, max(k, 1)), dtype=torch.int64, device=x2.device)
     else:
         vals, idx = out
+        _check_out(vals, (rows, k), torch.float32, x2.device, "out[0] (values)")
+        _check_out(idx, (rows, k), torch.int64, x2.device, "out[1] (indices)")
     stream = _stream_ptr(x2.device)
     ws, nb = workspace(a, rows, V, k, x2.device)
     st = load().osmx_softmax_topk(a, x2.data_ptr(), x2.stride(0), rows, V, k, vals.data_ptr(), idx.data_ptr(),
                                   ws.data_ptr(), ws.numel(), stream)
     _raise(st)
-    if check:
-        check_status(ws, stream)
+    _finish(ws, x2.device, stream, check)
     if x.dim() == 1:
         return vals[0], idx[0]
     return vals, idx
@@ -379,8 +428,7 @@ def proj_softmax_topk(h, w, k: int, check: bool = True):
     st = load().osmx_proj_softmax_topk(h.data_ptr(), rows, D, w.data_ptr(), V, k, vals.data_ptr(), idx.data_ptr(),
                                        ws.data_ptr(), ws.numel(), stream)
     _raise(st)
-    if check:
-        check_status(ws, stream)
+    _finish(ws, h.device, stream, check)
     return vals, idx
 
 
@@ -399,8 +447,7 @@ def topk(v, k: int, check: bool = True):
     st = load().osmx_topk(v2.data_ptr(), v2.stride(0), rows, V, k, vals.data_ptr(), idx.data_ptr(), ws.data_ptr(),
                           ws.numel(), stream)
     _raise(st)
-    if check:
-        check_status(ws, stream)
+    _finish(ws, v2.device, stream, check)
     if v.dim() == 1:
         return vals[0], idx[0]
     return vals, idx
@@ -421,8 +468,7 @@ def normalizer(x, chunk: int = 0, check: bool = True):
     st = load().osmx_normalizer(x2.data_ptr(), x2.stride(0), rows, V, chunk, m.data_ptr(), d.data_ptr(),
                                 ws.data_ptr(), ws.numel(), stream)
     _raise(st)
-    if check:
-        check_status(ws, stream)
+    _finish(ws, x2.device, stream, check)
     return m, d
 
 
@@ -446,6 +492,7 @@ def slice_record(x_slice, col0: int, k: int):
     ws = _ws.get(nb, x1.device, stream)
     st = load().osmx_slice_record(x1.data_ptr(), V, col0, k, rec.data_ptr(), ws.data_ptr(), ws.numel(), stream)
     _raise(st)
+    _ws.mark_dirty(x1.device, stream)  # non-finite slices poison the record; its flag is not checked here
     return rec
 
 
@@ -464,8 +511,7 @@ def records_combine(records, k: int, check: bool = True):
                                      vals.data_ptr() if k > 0 else None, idx.data_ptr() if k > 0 else None,
                                      ws.data_ptr(), ws.numel(), stream)
     _raise(st)
-    if check:
-        check_status(ws, stream)
+    _finish(ws, records.device, stream, check)
     return vals[:k], idx[:k], out_rec
 
 
