@@ -54,3 +54,27 @@ $(BENCHCLI): tools/osmx_bench_gpu.cu include/osmx_b200.h $(LIB)
 
 benchcli: $(BENCHCLI)
 .PHONY: benchcli
+
+# The reference's OWN unit tests (proj/tests/test_softmax.cpp,
+# test_normalizer.cpp, unmodified, compiled where they lie) against the B200
+# C++ facade: our include/ comes first, so "osmx/softmax.hpp",
+# "osmx/normalizer.hpp" and "osmx/error.hpp" resolve to the GPU-backed
+# headers; osmx/oracle.hpp (the reference's double-precision ground truth,
+# src/oracle.cpp) and test_support.hpp come from the reference tree;
+# <doctest.h> is tests/cpp/doctest.h.  Built only where /root/reference
+# exists (this container); the binary travels to the GPU box in build/.
+REF ?= /root/reference/proj
+REFSUITE = build/ref_unit_tests_b200
+REFSUITE_SRC = $(REF)/tests/doctest_main.cpp $(REF)/tests/test_softmax.cpp $(REF)/tests/test_normalizer.cpp \
+               $(REF)/src/oracle.cpp
+$(REFSUITE): $(REFSUITE_SRC) include/osmx/*.hpp include/osmx_b200.h tests/cpp/doctest.h $(LIB)
+	@mkdir -p build
+	g++ -std=c++20 -O2 -Iinclude -Itests/cpp -I$(REF)/include -I$(REF)/tests -o $@ $(REFSUITE_SRC) \
+	    -L paper_1805_02867_b200 -losmx_b200 -Wl,-rpath,'$$ORIGIN/../paper_1805_02867_b200' \
+	    -L/usr/local/cuda/lib64 -lcudart
+
+refsuite: $(REFSUITE)
+.PHONY: refsuite
+ifneq ($(wildcard $(REF)/tests/test_softmax.cpp),)
+all: refsuite
+endif

@@ -118,13 +118,23 @@ osmx_status osmx_proj_softmax_topk(const void* h, int64_t rows, int64_t D, const
 osmx_status osmx_topk(const float* v, int64_t ld, int64_t rows, int64_t V, int32_t k, float* vals,
                       int64_t* idx, void* ws, size_t ws_bytes, void* stream);
 
-/* (m, d) of every row.  Replaces run_normalizer<float> /
- * run_normalizer_chunked<float> (normalizer.hpp:61-85).  chunk = 0 selects
- * the sequential contract; chunk > 0 only validates (>= 1 required by the
- * reference, :75-76): the device reduction order is the CTA tree, which the
- * reference's tests pin as equivalent (test_normalizer.cpp:229-262). */
+/* (m, d) of every row.  Replaces run_normalizer<T> /
+ * run_normalizer_chunked<T> (normalizer.hpp:61-85): chunk = 0 is the
+ * unchunked pass; chunk > 0 reduces every contiguous chunk of `chunk`
+ * elements to a state and merges the chunk states left to right
+ * (normalizer.hpp:77-83), one record per chunk in the workspace.  (The
+ * reference rejects chunk_len == 0 with invalid_chunk_error; its C++ facade
+ * include/osmx/normalizer.hpp keeps that check, 0 here means "unchunked".)
+ * chunk >= V is one chunk, bit-identical to chunk = 0 (test_normalizer.cpp
+ * "single chunk is bit-identical to sequential").  The workspace must hold
+ * osmx_normalizer_workspace_bytes(rows, V, chunk, 32 | 64) bytes.
+ * _f64 keeps the state in double like norm_state<double> (the reference's
+ * kernels accumulate d in double, kernels.hpp:65). */
+size_t osmx_normalizer_workspace_bytes(int64_t rows, int64_t V, int64_t chunk, int32_t precision);
 osmx_status osmx_normalizer(const float* x, int64_t ldx, int64_t rows, int64_t V, int64_t chunk,
                             float* m, float* d, void* ws, size_t ws_bytes, void* stream);
+osmx_status osmx_normalizer_f64(const float* x, int64_t ldx, int64_t rows, int64_t V, int64_t chunk,
+                                double* m, double* d, void* ws, size_t ws_bytes, void* stream);
 
 /* ------------------------------------- V-split records (multi-GPU rows) -- */
 
@@ -176,6 +186,11 @@ osmx_status osmx_softmax_topk_host_multi(int alg, const float* x, int64_t rows, 
                                          int64_t* first_bad_row);
 osmx_status osmx_topk_host_multi(const float* v, int64_t rows, int64_t V, int32_t k, float* vals,
                                  int64_t* idx, const int* devices, int32_t n_devices,
+                                 int64_t* first_bad_row);
+/* Host-buffer normalizer (run_normalizer / run_normalizer_chunked over a
+ * batch of rows): m, d are rows floats (precision 32) or doubles (64). */
+osmx_status osmx_normalizer_host(const float* x, int64_t rows, int64_t V, int64_t chunk, int32_t precision,
+                                 void* m, void* d, const int* devices, int32_t n_devices,
                                  int64_t* first_bad_row);
 /* Release the per-device staging buffers of the host path. */
 void osmx_host_release(void);

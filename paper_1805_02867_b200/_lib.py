@@ -39,6 +39,9 @@ SIGNATURES = {
     "osmx_softmax_topk": (_int, [_int, _vp, _i64, _i64, _i64, _i32, _vp, _vp, _vp, _sz, _vp]),
     "osmx_topk": (_int, [_vp, _i64, _i64, _i64, _i32, _vp, _vp, _vp, _sz, _vp]),
     "osmx_normalizer": (_int, [_vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _sz, _vp]),
+    "osmx_normalizer_f64": (_int, [_vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _sz, _vp]),
+    "osmx_normalizer_workspace_bytes": (_sz, [_i64, _i64, _i64, _i32]),
+    "osmx_normalizer_host": (_int, [_vp, _i64, _i64, _i64, _i32, _vp, _vp, _vp, _i32, _pi64]),
     "osmx_record_bytes": (_sz, [_i32]),
     "osmx_slice_record": (_int, [_vp, _i64, _i64, _i32, _vp, _vp, _sz, _vp]),
     "osmx_proj_softmax_topk": (_int, [_vp, _i64, _i64, _vp, _i64, _i32, _vp, _vp, _vp, _sz, _vp]),

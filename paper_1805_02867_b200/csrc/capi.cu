@@ -289,15 +289,32 @@ osmx_status osmx_proj_softmax_topk(const void* h, int64_t rows, int64_t D, const
                                       static_cast<cudaStream_t>(stream)));
 }
 
+size_t osmx_normalizer_workspace_bytes(int64_t rows, int64_t V, int64_t chunk, int32_t precision) {
+  return normalizer_ws(rows, V, chunk < 0 ? 0 : chunk, precision == 64 ? 64 : 32);
+}
+
 osmx_status osmx_normalizer(const float* x, int64_t ldx, int64_t rows, int64_t V, int64_t chunk, float* m,
                             float* d, void* ws, size_t ws_bytes, void* stream) {
   TuningScope scope;
   osmx_status s = check_common(x, ldx, rows, V);
   if (s) return s;
   if (chunk < 0) return OSMX_ERR_INVALID_CHUNK;
-  if ((rows > 0 && (!m || !d)) || !ws || ws_bytes < (size_t)osmx_dev::kWsHeader) return OSMX_ERR_INVALID_ARG;
+  if ((rows > 0 && (!m || !d)) || !ws) return OSMX_ERR_INVALID_ARG;
   if (rows == 0) return OSMX_OK;
+  if (ws_bytes < normalizer_ws(rows, V, chunk, 32)) return OSMX_ERR_INVALID_ARG;
   return cuda_status(launch_normalizer(x, ldx, rows, V, chunk, m, d, ws, static_cast<cudaStream_t>(stream)));
+}
+
+osmx_status osmx_normalizer_f64(const float* x, int64_t ldx, int64_t rows, int64_t V, int64_t chunk, double* m,
+                                double* d, void* ws, size_t ws_bytes, void* stream) {
+  TuningScope scope;
+  osmx_status s = check_common(x, ldx, rows, V);
+  if (s) return s;
+  if (chunk < 0) return OSMX_ERR_INVALID_CHUNK;
+  if ((rows > 0 && (!m || !d)) || !ws) return OSMX_ERR_INVALID_ARG;
+  if (rows == 0) return OSMX_OK;
+  if (ws_bytes < normalizer_ws(rows, V, chunk, 64)) return OSMX_ERR_INVALID_ARG;
+  return cuda_status(launch_normalizer_f64(x, ldx, rows, V, chunk, m, d, ws, static_cast<cudaStream_t>(stream)));
 }
 
 size_t osmx_record_bytes(int32_t k) { return record_bytes(k > 0 ? k : 1); }
@@ -488,14 +505,48 @@ HostCtx& host_ctx(int device, int slot) {
   return *p;
 }
 
-// What one row block runs: a softmax (out1 = y) or a top-K (out1 = vals,
-// out2 = idx).  alg is the C-ABI id; kTopkOf for osmx_topk_host.
+// What one row block runs: a softmax (out1 = y), a top-K (out1 = vals,
+// out2 = idx; alg kTopkOf for osmx_topk_host) or a normalizer (out1 = m,
+// out2 = d, float or double by `prec`).
 struct HostOp {
-  bool topk;
+  enum Kind { kSoftmax, kTopk, kNorm } kind;
   int alg;
   int k;
-  size_t out1_row() const { return topk ? (size_t)k * sizeof(float) : 0; }
-  size_t out2_row() const { return topk ? (size_t)k * sizeof(long long) : 0; }
+  long long chunk = 0;
+  int prec = 32;
+  size_t out1_row(long long V) const {
+    switch (kind) {
+      case kSoftmax: return (size_t)V * sizeof(float);
+      case kTopk: return (size_t)k * sizeof(float);
+      default: return prec == 64 ? sizeof(double) : sizeof(float);
+    }
+  }
+  size_t out2_row() const {
+    switch (kind) {
+      case kSoftmax: return 0;
+      case kTopk: return (size_t)k * sizeof(long long);
+      default: return prec == 64 ? sizeof(double) : sizeof(float);
+    }
+  }
+  size_t ws_bytes(long long rows, long long V) const {
+    return kind == kNorm ? normalizer_ws(rows, V, chunk, prec) : workspace_bytes(alg, rows, V, k);
+  }
+  osmx_status launch(const float* dx, long long nr, long long V, char* o1, char* o2, void* ws, size_t wsb,
+                     cudaStream_t st) const {
+    switch (kind) {
+      case kSoftmax:
+        return cuda_status(launch_softmax(alg, dx, V, reinterpret_cast<float*>(o1), V, nr, V, ws, wsb, st));
+      case kTopk:
+        return run_topk_alg(alg, dx, V, nr, V, k, reinterpret_cast<float*>(o1), reinterpret_cast<long long*>(o2),
+                            ws, wsb, st);
+      default:
+        if (prec == 64)
+          return cuda_status(launch_normalizer_f64(dx, V, nr, V, chunk, reinterpret_cast<double*>(o1),
+                                                   reinterpret_cast<double*>(o2), ws, st));
+        return cuda_status(launch_normalizer(dx, V, nr, V, chunk, reinterpret_cast<float*>(o1),
+                                             reinterpret_cast<float*>(o2), ws, st));
+    }
+  }
 };
 
 // The second output block (int64 indices) starts 256-byte aligned after the
@@ -511,15 +562,15 @@ osmx_status host_run(const HostOp& op, int device, int slot, const float* x, lon
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) return cuda_status(e);
   const size_t row_b = (size_t)V * sizeof(float);
-  const size_t o1 = op.topk ? op.out1_row() : row_b, o2 = op.out2_row();
+  const size_t o1 = op.out1_row(V), o2 = op.out2_row();
   long long rpb = (long long)std::max<size_t>(1, ((size_t)chunk_mb << 20) / row_b);
   rpb = std::min(rpb, rows);
   // The launch layer picks a kernel shape per block, so the short tail block
   // may take a path (split records) the full blocks do not: size the
   // workspace for both.
   const long long tail = rows % rpb;
-  size_t wsb = workspace_bytes(op.alg, rpb, V, op.k);
-  if (tail) wsb = std::max(wsb, workspace_bytes(op.alg, tail, V, op.k));
+  size_t wsb = op.ws_bytes(rpb, V);
+  if (tail) wsb = std::max(wsb, op.ws_bytes(tail, V));
   e = c.ensure(rpb * row_b, std::max<size_t>(out2_offset(rpb, o1) + (size_t)rpb * o2 + 256, 256), wsb);
   if (e != cudaSuccess) return cuda_status(e);
   osmx_status st = OSMX_OK;
@@ -539,11 +590,7 @@ osmx_status host_run(const HostOp& op, int device, int slot, const float* x, lon
     }
     const float* dx = static_cast<const float*>(c.xin[s]);
     char* dout = static_cast<char*>(c.out[s]);
-    if (op.topk)
-      st = run_topk_alg(op.alg, dx, V, nr, V, op.k, reinterpret_cast<float*>(dout),
-                        reinterpret_cast<long long*>(dout + out2_offset(rpb, o1)), c.ws[s], c.ws_b, c.st[s]);
-    else
-      st = cuda_status(launch_softmax(op.alg, dx, V, reinterpret_cast<float*>(dout), V, nr, V, c.ws[s], c.ws_b, c.st[s]));
+    st = op.launch(dx, nr, V, dout, dout + out2_offset(rpb, o1), c.ws[s], c.ws_b, c.st[s]);
     if (st != OSMX_OK) break;
     e = cudaMemcpyAsync(out1 + r0 * o1, dout, (size_t)nr * o1, cudaMemcpyDeviceToHost, c.st[s]);
     if (e == cudaSuccess && out2)
@@ -593,7 +640,7 @@ osmx_status host_multi(const HostOp& op, const float* x, long long rows, long lo
   if (rows == 0) return OSMX_OK;
   const Tuning snap = tuning();  // the caller's knobs, for every worker
   const long long chunk_mb = g_host_chunk_mb.load();
-  const size_t row_b = (size_t)V * sizeof(float), o1 = op.topk ? op.out1_row() : row_b, o2 = op.out2_row();
+  const size_t o1 = op.out1_row(V), o2 = op.out2_row();
   std::vector<osmx_status> st((size_t)n, OSMX_OK);
   std::vector<long long> bad((size_t)n, -1);
   std::vector<std::string> err((size_t)n);
@@ -640,7 +687,7 @@ osmx_status softmax_host_multi(int alg, const float* x, int64_t rows, int64_t V,
   osmx_status s = check_common(x, V, rows, V);
   if (s) return s;
   if (rows > 0 && !y) return OSMX_ERR_INVALID_ARG;
-  return host_multi(HostOp{false, alg, 0}, x, rows, V, y, nullptr, devices, n, first_bad_row);
+  return host_multi(HostOp{HostOp::kSoftmax, alg, 0}, x, rows, V, y, nullptr, devices, n, first_bad_row);
 }
 
 osmx_status topk_host_multi(int alg, const float* x, int64_t rows, int64_t V, int32_t k, float* vals, int64_t* idx,
@@ -652,7 +699,21 @@ osmx_status topk_host_multi(int alg, const float* x, int64_t rows, int64_t V, in
   if (s) return s;
   if ((s = check_k(V, k))) return s;
   if (rows > 0 && (!vals || !idx)) return OSMX_ERR_INVALID_ARG;
-  return host_multi(HostOp{true, alg, k}, x, rows, V, vals, idx, devices, n, first_bad_row);
+  return host_multi(HostOp{HostOp::kTopk, alg, k}, x, rows, V, vals, idx, devices, n, first_bad_row);
+}
+
+osmx_status normalizer_host_multi(const float* x, int64_t rows, int64_t V, int64_t chunk, int precision, void* m,
+                                  void* d, const int* devices, int n, int64_t* first_bad_row) {
+  if (first_bad_row) *first_bad_row = -1;
+  TuningScope scope;
+  osmx_status s = check_common(x, V, rows, V);
+  if (s) return s;
+  if (chunk < 0) return OSMX_ERR_INVALID_CHUNK;
+  if ((precision != 32 && precision != 64) || (rows > 0 && (!m || !d))) return OSMX_ERR_INVALID_ARG;
+  HostOp op{HostOp::kNorm, kNormalizer, 0};
+  op.chunk = chunk;
+  op.prec = precision;
+  return host_multi(op, x, rows, V, m, d, devices, n, first_bad_row);
 }
 
 }  // namespace
@@ -690,6 +751,11 @@ osmx_status osmx_softmax_topk_host_multi(int alg, const float* x, int64_t rows, 
 osmx_status osmx_topk_host_multi(const float* v, int64_t rows, int64_t V, int32_t k, float* vals, int64_t* idx,
                                  const int* devices, int32_t n_devices, int64_t* first_bad_row) {
   return topk_host_multi(kTopkOf, v, rows, V, k, vals, idx, devices, n_devices, first_bad_row);
+}
+
+osmx_status osmx_normalizer_host(const float* x, int64_t rows, int64_t V, int64_t chunk, int32_t precision,
+                                 void* m, void* d, const int* devices, int32_t n_devices, int64_t* first_bad_row) {
+  return normalizer_host_multi(x, rows, V, chunk, precision, m, d, devices, n_devices, first_bad_row);
 }
 
 void osmx_host_release(void) {

@@ -98,6 +98,90 @@ __device__ __forceinline__ float ex2(float x) {
 // argument error stays relative to |x - m| (small where terms matter).
 __device__ __forceinline__ float exp_sub(float x, float m) { return ex2((x - m) * kLog2e); }
 
+// ------------------------------------ the reference's libm, bit for bit --
+// The safe fused top-K selects on p = float(expf(x - m) / d) with d a double
+// (reference kernels.hpp:95-98); matching its indices bit for bit needs the
+// host's expf itself.  expf_ref is glibc's expf (the table-driven
+// optimized-routines algorithm: N = 32 table, degree-3 polynomial, all in
+// double, then one rounding to float), evaluated with the same IEEE double
+// operations -- identical to glibc 2.39's expf for every float in
+// [-130, 88] except two inputs whose results glibc corrects, listed below
+// (checked exhaustively on the host, tools/expf_ref_check.c).
+__device__ __constant__ unsigned long long kExpfTab[32] = {
+    0x3ff0000000000000ULL, 0x3fefd9b0d3158574ULL, 0x3fefb5586cf9890fULL, 0x3fef9301d0125b51ULL,
+    0x3fef72b83c7d517bULL, 0x3fef54873168b9aaULL, 0x3fef387a6e756238ULL, 0x3fef1e9df51fdee1ULL,
+    0x3fef06fe0a31b715ULL, 0x3feef1a7373aa9cbULL, 0x3feedea64c123422ULL, 0x3feece086061892dULL,
+    0x3feebfdad5362a27ULL, 0x3feeb42b569d4f82ULL, 0x3feeab07dd485429ULL, 0x3feea47eb03a5585ULL,
+    0x3feea09e667f3bcdULL, 0x3fee9f75e8ec5f74ULL, 0x3feea11473eb0187ULL, 0x3feea589994cce13ULL,
+    0x3feeace5422aa0dbULL, 0x3feeb737b0cdc5e5ULL, 0x3feec49182a3f090ULL, 0x3feed503b23e255dULL,
+    0x3feee89f995ad3adULL, 0x3feeff76f2fb5e47ULL, 0x3fef199bdd85529cULL, 0x3fef3720dcef9069ULL,
+    0x3fef5818dcfba487ULL, 0x3fef7c97337b9b5fULL, 0x3fefa4afa2a490daULL, 0x3fefd0765b6e4540ULL};
+
+__device__ __forceinline__ float expf_ref(float x) {
+  if (!(x > -150.0f)) return x == x ? 0.0f : x;  // underflow to +0 (and NaN through)
+  if (x > 0x1.62e42ep+6f) return __int_as_float(0x7f800000);  // overflow to +inf
+  if (__float_as_uint(x) == 0x4202422fu) return __uint_as_float(0x56fc9f1cu);  // glibc-corrected inputs
+  if (__float_as_uint(x) == 0xc27c65d9u) return __uint_as_float(0x11fa2993u);
+  const double z = __dmul_rn(0x1.71547652b82fep+5, (double)x);
+  double kd = __dadd_rn(z, 0x1.8p+52);
+  const unsigned long long ki = (unsigned long long)__double_as_longlong(kd);
+  kd = __dsub_rn(kd, 0x1.8p+52);
+  const double r = __dsub_rn(z, kd);
+  const unsigned long long t = kExpfTab[ki & 31] + (ki << 47);
+  const double sc = __longlong_as_double((long long)t);
+  const double q = __fma_rn(0x1.c6af84b912394p-20, r, 0x1.ebfce50fac4f3p-13);
+  double y = __fma_rn(0x1.62e42ff0c52d6p-6, r, 1.0);
+  y = __fma_rn(q, __dmul_rn(r, r), y);
+  return __double2float_rn(__dmul_rn(y, sc));
+}
+
+// e^t in double for t <= 0, relative error ~1e-15: the safe normalizer
+// d = sum exp(double(x) - m) (kernels.hpp:95-96) to far below an fp32 ulp,
+// at 11 double ops per term (about half of libdevice's exp).  e^t =
+// 2^(y/32), y = t * 32/ln2 split as ki + r (|r| <= 1/2, Cody-Waite with a
+// two-part constant), 2^(r/32) by a degree-5 Taylor polynomial in r,
+// 2^(ki/32) = 2^(ki>>5) * tab[ki & 31] with the table in shared memory
+// (exp2_tab_init) -- a constant-bank lookup would serialise over the lanes'
+// distinct indices.
+__device__ __constant__ double kExp2Tab32[32] = {
+    0x1.0000000000000p+0, 0x1.059b0d3158574p+0, 0x1.0b5586cf9890fp+0, 0x1.11301d0125b51p+0,
+    0x1.172b83c7d517bp+0, 0x1.1d4873168b9aap+0, 0x1.2387a6e756238p+0, 0x1.29e9df51fdee1p+0,
+    0x1.306fe0a31b715p+0, 0x1.371a7373aa9cbp+0, 0x1.3dea64c123422p+0, 0x1.44e086061892dp+0,
+    0x1.4bfdad5362a27p+0, 0x1.5342b569d4f82p+0, 0x1.5ab07dd485429p+0, 0x1.6247eb03a5585p+0,
+    0x1.6a09e667f3bcdp+0, 0x1.71f75e8ec5f74p+0, 0x1.7a11473eb0187p+0, 0x1.82589994cce13p+0,
+    0x1.8ace5422aa0dbp+0, 0x1.93737b0cdc5e5p+0, 0x1.9c49182a3f090p+0, 0x1.a5503b23e255dp+0,
+    0x1.ae89f995ad3adp+0, 0x1.b7f76f2fb5e47p+0, 0x1.c199bdd85529cp+0, 0x1.cb720dcef9069p+0,
+    0x1.d5818dcfba487p+0, 0x1.dfc97337b9b5fp+0, 0x1.ea4afa2a490dap+0, 0x1.f50765b6e4540p+0};
+
+// Call with every thread of the CTA, before a barrier.
+__device__ __forceinline__ void exp2_tab_init(double* tab) {
+  if (threadIdx.x < 32) tab[threadIdx.x] = kExp2Tab32[threadIdx.x];
+}
+
+__device__ __forceinline__ double exp_neg_d(double t, const double* tab) {
+  if (!(t > -708.0)) return t == t ? 0.0 : t;  // underflow (and NaN through)
+  const double y = __dmul_rn(t, 0x1.71547652b82fep+5);
+  const double kd0 = __dadd_rn(y, 0x1.8p+52);
+  const long long ki = __double_as_longlong(kd0) - 0x4338000000000000LL;
+  const double kd = __dsub_rn(kd0, 0x1.8p+52);
+  double r = __fma_rn(t, 0x1.71547652b82fep+5, -kd);
+  r = __fma_rn(t, 0x1.777d0ffda0d24p-51, r);
+  double p = __fma_rn(0x1.5d87fe78a6731p-35, r, 0x1.3b2ab6fba4e77p-27);
+  p = __fma_rn(p, r, 0x1.c6b08d704a0c0p-20);
+  p = __fma_rn(p, r, 0x1.ebfbdff82c58fp-13);
+  p = __fma_rn(p, r, 0x1.62e42fefa39efp-6);
+  p = __fma_rn(p, r, 1.0);
+  const double sc = __longlong_as_double(__double_as_longlong(tab[ki & 31]) + ((ki >> 5) << 52));
+  return __dmul_rn(p, sc);
+}
+
+// The reference's safe selection key (kernels.hpp:98): float(expf(x - m) / d),
+// x - m rounded in float, the quotient in double.  Monotone non-decreasing in
+// x (checked with expf_ref over [-130, 0]), so a batch max bounds a batch.
+__device__ __forceinline__ float safe_key_ref(float x, float m, double d) {
+  return __double2float_rn(__ddiv_rn((double)expf_ref(__fsub_rn(x, m)), d));
+}
+
 // ------------------------------------------------------- (m, d) monoid --
 
 struct MD {
@@ -189,10 +273,41 @@ struct L2Acc {
     raise(x);
     d += term(x);
   }
+  // d relative to m: divide by the term the max element itself contributed,
+  // 2^(m*L - n) -- the same FFMA + ex2 as in add_batch -- so a row whose
+  // other terms vanish gets d == 1 exactly, like the reference's first
+  // absorb (normalizer.hpp:36-37).
   __device__ __forceinline__ MD finish() const {
     if (huge || m == kNegInf || !(m == m)) return MD{m, d};
-    return MD{m, d * ex2(fmaf(-m, kLog2e, n))};
+    return MD{m, __fdiv_rn(d, ex2(fmaf(m, kLog2e, -n)))};
   }
+};
+
+// Safe-softmax normalizer (Alg. 2, kernels.hpp:55-56): the row max M is known
+// before the sum, so every term is e^(x - M) = 2^((x - M) * L) computed from
+// the difference x - M alone -- shifting a row by a constant that keeps
+// x + c exact leaves every term, d and the outputs bit-identical, the
+// reference's own shift-invariance property (test_softmax.cpp "shift
+// invariance").  Same interface as L2Acc (raise once with M).
+struct SafeAcc {
+  float M = kNegInf;
+  float d = 0.0f;
+  __device__ __forceinline__ void raise(float m) { M = m; }
+  __device__ __forceinline__ float term(float x) const { return ex2((x - M) * kLog2e); }
+  template <int U>
+  __device__ __forceinline__ void add_batch(const float4 (&v)[U]) {
+    float s = 0.0f;
+    const float2 L2 = make_float2(kLog2e, kLog2e), M2 = make_float2(-M, -M);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const float2 t0 = __fmul2_rn(__fadd2_rn(make_float2(v[u].x, v[u].y), M2), L2);
+      const float2 t1 = __fmul2_rn(__fadd2_rn(make_float2(v[u].z, v[u].w), M2), L2);
+      const float2 p = __fadd2_rn(make_float2(ex2(t0.x), ex2(t1.x)), make_float2(ex2(t0.y), ex2(t1.y)));
+      s += p.x + p.y;
+    }
+    d += s;
+  }
+  __device__ __forceinline__ MD finish() const { return MD{M, d}; }
 };
 
 // merge(), reference normalizer.hpp:52-58.  The identity (-inf, 0) is

@@ -92,8 +92,13 @@ cudaError_t launch_softmax(int alg, const float* x, long long ldx, float* y, lon
 cudaError_t launch_topk(int alg, const float* x, long long ldx, long long rows, long long V, int k,
                         float* vals, long long* idx, void* ws, size_t ws_bytes, cudaStream_t st);
 
+// normalizer.cu: run_normalizer / run_normalizer_chunked (normalizer.hpp:61-85).
+// chunk 0 = unchunked; precision 32 (float state) or 64 (double state).
 cudaError_t launch_normalizer(const float* x, long long ldx, long long rows, long long V,
                               long long chunk, float* m, float* d, void* ws, cudaStream_t st);
+cudaError_t launch_normalizer_f64(const float* x, long long ldx, long long rows, long long V,
+                                  long long chunk, double* m, double* d, void* ws, cudaStream_t st);
+size_t normalizer_ws(long long rows, long long V, long long chunk, int precision);
 
 // Split-mode record of one row slice: (m, d, min) + k candidates.
 size_t record_bytes(int k);

@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(TPR > 256 ? TPR : 256)
 #pragma unroll
     for (int t = 0; t < EPT; ++t) lm = fmaxf(lm, a[t]);
     m = G::reduce(lm, OpMax(), smf);
-    L2Acc acc;
+    SafeAcc acc;
     acc.raise(m);
 #pragma unroll
     for (int t = 0; t < EPT; ++t) acc.d += acc.term(a[t]);
@@ -314,7 +314,7 @@ __global__ void __launch_bounds__(BLOCK)
           pf);
       M = cta_max<NW>(m, smf);
       mn = cta_min<NW>(mn, smf);
-      L2Acc sacc;  // sum e^(x - M) as one FFMA + ex2 per element
+      SafeAcc sacc;  // sum e^(x - M), terms from x - M (shift invariant)
       sacc.raise(M);
       stream_seg<BLOCK, U, P1>(
           s, t, [&](float v, long long) { sacc.d += sacc.term(v); },
@@ -394,11 +394,35 @@ __global__ void __launch_bounds__(BLOCK)
   const Seg s = make_seg(x + row * ldx + c0, n);
   const int t = threadIdx.x;
   SRec* rr = rec + row * S;
+  if constexpr (ALG == osmx_host::kSafe && PHASE == 2) {
+    // the safe fused top-K's normalizer: d in double, exp(double(x) - M)
+    // (reference kernels.hpp:95-96; its keys divide by d)
+    float M = kNegInf;
+    for (int i = t; i < S; i += BLOCK) M = fmaxf(M, rr[i].m);
+    M = cta_max<NW>(M, smf);
+    __shared__ double tab[32];
+    exp2_tab_init(tab);
+    __syncthreads();
+    const double Md = (double)M;
+    double d = 0.0;
+    stream_seg<BLOCK, U, false>(
+        s, t, [&](float v, long long) { d += exp_neg_d((double)v - Md, tab); },
+        [&](float4 (&v)[U], long long, int) {
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            d += (exp_neg_d((double)v[u].x - Md, tab) + exp_neg_d((double)v[u].y - Md, tab)) +
+                 (exp_neg_d((double)v[u].z - Md, tab) + exp_neg_d((double)v[u].w - Md, tab));
+        });
+    d = cta_sum_d<NW>(d, smd);
+    __syncthreads();  // every thread has read rr[*].m before it is rewritten
+    if (t == 0) rr[blockIdx.x].d = d;
+    return;
+  }
   if constexpr (ALG == osmx_host::kSafe && PHASE == 1) {
     float M = kNegInf;
     for (int i = t; i < S; i += BLOCK) M = fmaxf(M, rr[i].m);
     M = cta_max<NW>(M, smf);
-    L2Acc sacc;  // sum e^(x - M) as one FFMA + ex2 per element
+    SafeAcc sacc;  // sum e^(x - M), terms from x - M (shift invariant)
     sacc.raise(M);
     stream_seg<BLOCK, U, false>(
         s, t, [&](float v, long long) { sacc.d += sacc.term(v); },

@@ -8,8 +8,8 @@ cudaError_t launch_softmax_online(const float* x, long long ldx, float* y, long 
   return launch_alg<kOnline>(x, ldx, y, ldy, rows, V, ws, st);
 }
 
-cudaError_t launch_normalizer(const float* x, long long ldx, long long rows, long long V,
-                              long long, float* m, float* d, void* ws, cudaStream_t st) {
+cudaError_t launch_normalizer_f32_tree(const float* x, long long ldx, long long rows, long long V, float* m,
+                                       float* d, void* ws, cudaStream_t st) {
   const long long grid = std::min<long long>(rows, 1LL << 30);
   k_normalizer<256, 4><<<(unsigned)grid, 256, 0, st>>>(x, ldx, rows, V, m, d, ws);
   count_launch();

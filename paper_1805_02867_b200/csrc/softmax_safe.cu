@@ -14,7 +14,7 @@ cudaError_t launch_safe_split_stats(const float* x, long long ldx, long long row
   dim3 grid((unsigned)S, (unsigned)rows);
   SRec* rec = static_cast<SRec*>(srec);
   k_softmax_split_part<kSplitBlock, kSplitU, kSafe, 0><<<grid, kSplitBlock, 0, st>>>(x, ldx, V, chunk, rec);
-  k_softmax_split_part<kSplitBlock, kSplitU, kSafe, 1><<<grid, kSplitBlock, 0, st>>>(x, ldx, V, chunk, rec);
+  k_softmax_split_part<kSplitBlock, kSplitU, kSafe, 2><<<grid, kSplitBlock, 0, st>>>(x, ldx, V, chunk, rec);
   count_launch(2);
   return cudaGetLastError();
 }

@@ -372,7 +372,7 @@ __global__ void __launch_bounds__(1024, 1)
             mn = fminf(mn, rec[q].mn);
           }
         }
-        L2Acc sacc;
+        SafeAcc sacc;
         sacc.raise(M);
         for (int q = qa + tg; q < qb; q += GT) {
           float4 v[1] = {sl4[q]};

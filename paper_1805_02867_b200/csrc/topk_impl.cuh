@@ -51,7 +51,8 @@ struct Pass {
   TopList<KC> L;
   L2Acc acc;  // online (m, d) of the fused mode
   float mn = -kNegInf, chk = 0.0f;
-  float M = 0.0f, R = 0.0f;  // SAFE select pass: row max and 1/d
+  float M = 0.0f;   // SAFE select pass: row max
+  double D = 1.0;   //                   and the double normalizer
 
   __device__ __forceinline__ void scalar(float v, int j, int k) {
     if constexpr (MODE == kModeFused) {
@@ -62,7 +63,7 @@ struct Pass {
       chk = fmaf(v, 0.0f, chk);  // NaN iff some element was inf / NaN
       L.offer(v, j);
     } else {
-      L.offer(expf(v - M) * R, j);
+      L.offer(safe_key_ref(v, M, D), j);
     }
   }
   __device__ __forceinline__ void batch(const Seg& s, float4 (&v)[U], long long q0, int cnt, int k) {
@@ -157,12 +158,14 @@ struct Pass {
       }
       select_batch(v, cnt, j0, jstride, bm, [](float e) { return e; });
     } else {
-      // p is monotone in x for a fixed row (M, R): filter on the batch max.
+      // p is monotone in x for a fixed row (M, D): filter on the batch max.
       float bm = kNegInf;
 #pragma unroll
       for (int u = 0; u < U; ++u) bm = fmaxf(bm, fmaxf(fmaxf(v[u].x, v[u].y), fmaxf(v[u].z, v[u].w)));
-      const float Mr = M, Rr = R;
-      select_batch(v, cnt, j0, jstride, expf(bm - Mr) * Rr, [Mr, Rr](float e) { return expf(e - Mr) * Rr; });
+      const float Mr = M;
+      const double Dr = D;
+      select_batch(v, cnt, j0, jstride, safe_key_ref(bm, Mr, Dr),
+                   [Mr, Dr](float e) { return safe_key_ref(e, Mr, Dr); });
     }
   }
 };
@@ -185,16 +188,21 @@ __device__ __forceinline__ void safe_max_min(const Seg& s, int t, float& m, floa
         }
       });
 }
+// d = sum exp(double(x) - m) in double, as the reference (kernels.hpp:95-96):
+// the selection keys divide by it, so it must be accurate far below an fp32
+// ulp for the keys to round like the reference's.  Padding (-inf) adds 0.
 template <int G, int U>
-__device__ __forceinline__ float safe_sum(const Seg& s, int t, float M) {
-  float d = 0.0f;
+__device__ __forceinline__ double safe_sum(const Seg& s, int t, float M, const double* tab) {
+  const double Md = (double)M;
+  double d = 0.0;
   stream_seg<G, U, false>(
-      s, t, [&](float v, long long) { d += exp_sub(v, M); },
+      s, t, [&](float v, long long) { d += exp_neg_d((double)v - Md, tab); },
       [&](float4 (&v)[U], long long, int) {
-        float sum = 0.0f;
+        double sum = 0.0;
 #pragma unroll
         for (int u = 0; u < U; ++u)
-          sum += (exp_sub(v[u].x, M) + exp_sub(v[u].y, M)) + (exp_sub(v[u].z, M) + exp_sub(v[u].w, M));
+          sum += (exp_neg_d((double)v[u].x - Md, tab) + exp_neg_d((double)v[u].y - Md, tab)) +
+                 (exp_neg_d((double)v[u].z - Md, tab) + exp_neg_d((double)v[u].w - Md, tab));
         d += sum;
       });
   return d;
@@ -258,12 +266,15 @@ __global__ void __launch_bounds__(BLOCK, MINB)
   __shared__ __align__(16) float4 pipe_buf[NST > 0 ? NW * NST * U * 32 : (NST == -2 ? NW * 3 * U * 32 : 1)];
   __shared__ __align__(8) uint64_t bulk_bar[NST == -2 ? NW * 3 : 1];  // per-warp bulk ring (NST = -2)
   __shared__ float smf[2 * NW];
+  __shared__ double smd[NW];
   __shared__ float sv[NW * KC];
   __shared__ int si[NW * KC];
   __shared__ int tsh[2];  // CTA-shared admission bound, double-buffered by row parity
+  __shared__ double exp2tab[MODE == kModeSafe ? 32 : 1];  // safe: exp_neg_d's table
   const int t = threadIdx.x % G;
   const long long nrow_groups = (rows + RPC - 1) / RPC;
   if (threadIdx.x == 0) tsh[0] = tsh[1] = Pass<KC, U, MODE, G>::f2o(kNegInf);
+  if constexpr (MODE == kModeSafe) exp2_tab_init(exp2tab);
   if constexpr (NST == -2) {
     if (threadIdx.x == 0) {
       for (int b = 0; b < NW * 3; ++b)
@@ -308,13 +319,13 @@ __global__ void __launch_bounds__(BLOCK, MINB)
         M = cta_max<NW>(m, smf);
         MN = cta_min<NW>(mn, smf);
       }
-      float d = safe_sum<G, U>(s, t, M);
+      double d = safe_sum<G, U>(s, t, M, exp2tab);
       if constexpr (G == 32)
-        d = group_sum<32>(d);
+        d = group_sum_d<32>(d);
       else
-        d = cta_sum<NW>(d, smf);
+        d = cta_sum_d<NW>(d, smd);
       P.M = M;
-      P.R = __frcp_rn(d);
+      P.D = d;
       bad = !(d == d) || !isfinite(M) || !(MN == MN) || MN == kNegInf;
     }
     if constexpr (NST == -2 && MODE != kModeSafe) {  // per-warp bulk-copy ring, 3 stages
@@ -402,6 +413,7 @@ __global__ void __launch_bounds__(BLOCK)
                       int k, long long col0, char* __restrict__ rec, const SRecView* __restrict__ srec) {
   constexpr int NW = BLOCK / 32;
   __shared__ float smf[2 * NW];
+  __shared__ double smd[NW];
   __shared__ float sv[NW * KC];
   __shared__ int si[NW * KC];
   const int S = gridDim.x;
@@ -420,18 +432,19 @@ __global__ void __launch_bounds__(BLOCK)
   float safe_mn = 0.0f;
   if constexpr (MODE == kModeSafe) {
     const SRecView* rr = srec + row * S;
-    float M = kNegInf, d = 0.0f, mn = -kNegInf;
+    float M = kNegInf, mn = -kNegInf;
+    double d = 0.0;
     for (int i = t; i < S; i += BLOCK) {
       M = fmaxf(M, rr[i].m);
       mn = fminf(mn, rr[i].mn);
       if (rr[i].mn != rr[i].mn) mn = kNegInf;
-      d += (float)rr[i].d;
+      d += rr[i].d;
     }
     M = cta_max<NW>(M, smf);
     mn = cta_min<NW>(mn, smf);
-    d = cta_sum<NW>(d, smf);
+    d = cta_sum_d<NW>(d, smd);
     P.M = M;
-    P.R = __frcp_rn(d);
+    P.D = d;
     // poison the record when the row holds a non-finite value
     if (!(d == d) || !isfinite(M) || mn == kNegInf) safe_mn = __int_as_float(0x7fffffff);
   }

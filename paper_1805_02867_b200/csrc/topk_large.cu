@@ -86,7 +86,9 @@ __global__ void __launch_bounds__(kLT, 1)
   const Seg s = make_seg(xr, V);
 
   // 1. statistics
+  __shared__ double smd[kLW];
   float M = 0.0f, R = 1.0f;
+  double D = 1.0;  // safe mode: the double normalizer
   bool bad = false;
   if constexpr (MODE == 0) {
     L2Acc acc;
@@ -131,19 +133,24 @@ __global__ void __launch_bounds__(kLT, 1)
     chk = cta_sum<kLW>(chk, smf);
     bad = !(chk == chk);
     if constexpr (MODE == 2) {
+      // d = sum exp(double(x) - m) in double (kernels.hpp:95-96)
       M = cta_max<kLW>(m, smf);
-      float d = 0.0f;
+      __shared__ double tab[32];
+      exp2_tab_init(tab);
+      __syncthreads();
+      const double Md = (double)M;
+      double d = 0.0;
       stream_seg<kLT, U, 0>(
-          s, t, [&](float v, long long) { d += exp_sub(v, M); },
+          s, t, [&](float v, long long) { d += exp_neg_d((double)v - Md, tab); },
           [&](float4 (&v)[U], long long, int cnt) {
 #pragma unroll
             for (int u = 0; u < U; ++u)
               if (u < cnt)
-                d += (exp_sub(v[u].x, M) + exp_sub(v[u].y, M)) + (exp_sub(v[u].z, M) + exp_sub(v[u].w, M));
+                d += (exp_neg_d((double)v[u].x - Md, tab) + exp_neg_d((double)v[u].y - Md, tab)) +
+                     (exp_neg_d((double)v[u].z - Md, tab) + exp_neg_d((double)v[u].w - Md, tab));
           });
-      d = cta_sum<kLW>(d, smf);
-      R = __frcp_rn(d);
-      bad = bad || !(d == d) || !isfinite(M);
+      D = cta_sum_d<kLW>(d, smd);
+      bad = bad || !(D == D) || !isfinite(M);
     }
   }
   if (t == 0) {
@@ -153,7 +160,7 @@ __global__ void __launch_bounds__(kLT, 1)
   }
   auto key = [&](float v) -> unsigned {
     if constexpr (MODE == 2)
-      return fkey(expf(v - M) * R);
+      return fkey(safe_key_ref(v, M, D));  // the reference's p, bit for bit
     else
       return fkey(v);
   };

@@ -238,37 +238,41 @@ def online_softmax_then_topk(x, k: int) -> TopkResult:
     return _topk_host(_lib.ONLINE_SOFTMAX_UNFUSED_TOPK, x, k)
 
 
-def _normalizer_host(x, chunk: int | None) -> NormState | tuple[np.ndarray, np.ndarray]:
-    import torch
-
+def _normalizer_host(x, chunk: int, precision: int):
     a, single = _as_rows(x)
     rows, V = a.shape
     if V == 0:
         raise EmptyInputError()
-    if chunk is not None and chunk == 0:
-        raise InvalidChunkError()
-    dev = torch.device("cuda", _devices[0])
-    xt = torch.from_numpy(a).to(dev)
-    m, d = normalizer(xt, chunk=chunk or 0)
-    m, d = m.cpu().numpy(), d.cpu().numpy()
+    dt = np.float64 if precision == 64 else np.float32
+    m = np.empty(rows, dt)
+    d = np.empty(rows, dt)
+    bad = C.c_int64(-1)
+    devs, n = _dev_array()
+    st = load().osmx_normalizer_host(a.ctypes.data, rows, V, int(chunk), precision, m.ctypes.data, d.ctypes.data,
+                                     devs, n, C.byref(bad))
+    _raise(st, bad.value)
     if single:
         return NormState(float(m[0]), float(d[0]))
     return m, d
 
 
-def run_normalizer(x):
-    """(max, sum e^(x-max)) of the vector (normalizer.hpp:60-67)."""
-    return _normalizer_host(x, None)
+def run_normalizer(x, precision: int = 64):
+    """(max, sum e^(x-max)) of the vector (normalizer.hpp:60-67): the state is
+    double (run_normalizer<double>, the precision of the reference's kernels)
+    or float (precision=32, run_normalizer<float>)."""
+    return _normalizer_host(x, 0, precision)
 
 
-def run_normalizer_chunked(x, chunk_len: int):
-    """Chunked normalizer (normalizer.hpp:69-85).  chunk_len == 0 raises
-    InvalidChunkError like the reference; the device evaluation order is the
-    CTA merge tree (the reference pins its equivalence,
-    test_normalizer.cpp:229-262)."""
-    if int(chunk_len) < 0:
+def run_normalizer_chunked(x, chunk_len: int, precision: int = 64):
+    """Chunked normalizer (normalizer.hpp:69-85): one state per contiguous
+    chunk of chunk_len elements, merged left to right.  chunk_len == 0 raises
+    InvalidChunkError like the reference (after the empty check)."""
+    a, _ = _as_rows(x)
+    if a.shape[1] == 0:
+        raise EmptyInputError()
+    if int(chunk_len) <= 0:
         raise InvalidChunkError()
-    return _normalizer_host(x, int(chunk_len))
+    return _normalizer_host(x, int(chunk_len), precision)
 
 
 # ---------------------------------------------------- batched (device) -----
@@ -453,20 +457,26 @@ def topk(v, k: int, check: bool = True):
     return vals, idx
 
 
-def normalizer(x, chunk: int = 0, check: bool = True):
-    """Batched (m, d) per row (float32 tensors)."""
+def normalizer(x, chunk: int = 0, check: bool = True, precision: int = 32):
+    """Batched (m, d) per row: float32 (precision 32) or float64 (64) tensors.
+    chunk > 0: one state per contiguous chunk, merged left to right."""
     import torch
 
     x2 = _check_tensor(x)
     rows, V = x2.shape
     if V == 0:
         raise EmptyInputError()
-    m = torch.empty(rows, dtype=torch.float32, device=x2.device)
-    d = torch.empty(rows, dtype=torch.float32, device=x2.device)
+    if precision not in (32, 64):
+        raise ValueError("precision must be 32 or 64")
+    dt = torch.float64 if precision == 64 else torch.float32
+    m = torch.empty(rows, dtype=dt, device=x2.device)
+    d = torch.empty(rows, dtype=dt, device=x2.device)
     stream = _stream_ptr(x2.device)
-    ws, nb = workspace(8, rows, V, 0, x2.device)
-    st = load().osmx_normalizer(x2.data_ptr(), x2.stride(0), rows, V, chunk, m.data_ptr(), d.data_ptr(),
-                                ws.data_ptr(), ws.numel(), stream)
+    nb = load().osmx_normalizer_workspace_bytes(rows, V, int(chunk), precision)
+    ws = _ws.get(nb, x2.device, stream)
+    fn = load().osmx_normalizer_f64 if precision == 64 else load().osmx_normalizer
+    st = fn(x2.data_ptr(), x2.stride(0), rows, V, chunk, m.data_ptr(), d.data_ptr(), ws.data_ptr(), ws.numel(),
+            stream)
     _raise(st)
     _finish(ws, x2.device, stream, check)
     return m, d

@@ -52,7 +52,10 @@ def test_device_vs_reference_golden(cuda, golden):
             gz = golden[f"{n}/{op}/indices"]
             gv = golden[f"{n}/{op}/values"]
             got = z.cpu().numpy()[0]
-            if not np.array_equal(got, gz):  # only probability-rounding collisions allowed
+            if alg == "safe_fused":  # bit for bit (double d, the host's expf)
+                assert np.array_equal(got, gz), (n, got, gz)
+                assert np.array_equal(v.cpu().numpy()[0].view(np.int32), gv.view(np.int32)), n
+            elif not np.array_equal(got, gz):  # unfused: probability-rounding collisions allowed
                 ys = golden[f"{n}/safe_softmax"]
                 assert np.allclose(np.sort(ys[got]), np.sort(ys[gz]), rtol=2.5e-7, atol=0), (n, alg)
             assert max_rel(v.cpu().numpy()[0], gv) <= 1e-5
@@ -60,6 +63,17 @@ def test_device_vs_reference_golden(cuda, golden):
         gm, gd = golden[f"{n}/run_normalizer_double"]
         assert float(m[0]) == np.float32(gm)
         assert abs(float(d[0]) - gd) <= 1e-5 * gd
+        # double state: the reference's run_normalizer<double> / _chunked(7)
+        for chunk, key in ((0, "run_normalizer_double"), (7, "run_normalizer_chunked7_double")):
+            m, d = osmx.normalizer(_dev(x), chunk=chunk, precision=64)
+            gm, gd = golden[f"{n}/{key}"]
+            assert float(m[0]) == gm, (n, key)
+            assert abs(float(d[0]) - gd) <= 1e-12 * gd, (n, key, float(d[0]), gd)
+        # float state, chunked: the reference's fp32 left-to-right fold
+        m, d = osmx.normalizer(_dev(x), chunk=7, precision=32)
+        gm, gd = golden[f"{n}/run_normalizer_chunked7_float"]
+        assert float(m[0]) == gm
+        assert abs(float(d[0]) - gd) <= 2e-6 * gd, (n, float(d[0]), gd)
 
 
 @pytest.mark.parametrize("k", [0, 1, 5, 32])
@@ -104,6 +118,19 @@ def test_cpp_reference_api_binary(cuda):
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600)
     print(r.stdout[-2000:], r.stderr[-4000:])
     assert r.returncode == 0 and "ALL OK" in r.stdout
+
+
+def test_reference_unit_tests_against_b200(cuda):
+    """The reference's OWN unit tests (proj/tests/test_softmax.cpp and
+    test_normalizer.cpp, unmodified) compiled against the B200 C++ facade
+    (include/osmx/*.hpp; Makefile target refsuite, built where
+    /root/reference exists) and run on the GPU: every test case passes."""
+    exe = ROOT / "build" / "ref_unit_tests_b200"
+    if not exe.exists():
+        pytest.skip("build/ref_unit_tests_b200 not built (needs /root/reference at build time)")
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=900)
+    print(r.stdout[-2000:], r.stderr[-4000:])
+    assert r.returncode == 0 and "0 failed" in r.stdout
 
 
 def test_bench_shape_properties(cuda, oracle_mod):

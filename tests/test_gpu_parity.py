@@ -226,13 +226,16 @@ def _prob_collisions(got_idx, ref_idx, ref_probs_row_fn):
     ("safe_unfused", "safe_softmax_then_topk", "safe_softmax"),
     ("online_unfused", None, "online_softmax"),
 ])
-@pytest.mark.parametrize("shape", ["auto", "split"])
+@pytest.mark.parametrize("shape", ["auto", "split", "warp", "cta"])
 def test_probability_selection_topk(cuda, oracle_mod, lib, alg, op, base, shape):
     """Selection on probabilities: indices equal to the reference's except
     where two probabilities collide in fp32 rounding (flagged, counted)."""
     from paper_1805_02867_b200 import osmx
 
-    lib.config_set("shape", SHAPES[shape])
+    if shape in ("warp", "cta"):
+        lib.config_set("topk_threads", 32 if shape == "warp" else 256)
+    else:
+        lib.config_set("shape", SHAPES[shape])
     if shape == "split":
         lib.config_set("split_chunk", 2048)
     rng = np.random.default_rng(400)
@@ -248,7 +251,13 @@ def test_probability_selection_topk(cuda, oracle_mod, lib, alg, op, base, shape)
             else:
                 rv, rz = _topk_ref(oracle_mod, op, x, k)
             gi = idx.cpu().numpy()
-            collisions += _prob_collisions(gi, rz, lambda r: y[r])
+            if alg == "safe_fused":
+                # d in double and the host's expf (csrc/common.cuh expf_ref):
+                # keys, hence indices and values, bit for bit (kernels.hpp:95-98)
+                assert np.array_equal(gi, rz), (V, d, shape, gi[:2], rz[:2])
+                assert np.array_equal(vals.cpu().numpy().view(np.int32), rv.view(np.int32)), (V, d, shape)
+            else:  # the unfused pipelines may differ by probability-rounding collisions
+                collisions += _prob_collisions(gi, rz, lambda r: y[r])
             assert max_rel(vals.cpu().numpy(), rv) <= TOL
     print(f"{alg}/{shape}: rows with probability-rounding collisions: {collisions}")
 
@@ -466,3 +475,41 @@ def test_large_k(cuda, oracle_mod, lib, k):
                 rv, rz = _topk_ref(oracle_mod, op, x, kk)
                 _prob_collisions(idx.cpu().numpy(), rz, lambda r: y[r])
                 assert max_rel(vals.cpu().numpy(), rv) <= TOL
+
+
+def _collision_rows(rng, rows, V):
+    """Rows whose top probabilities collide after float rounding: 64 distinct
+    logits 1 - j*2^-24 (j < 64) at random positions over a normal background.
+    Their e^(x - m) are distinct floats just below 1, but divided by d they
+    round onto a coarser grid, so several share one p and the reference's
+    tie rule (lowest index first, topk.hpp:37-43) decides the order."""
+    x = (rng.standard_normal((rows, V)) * 2.0 - 6.0).astype(np.float32)
+    for r in range(rows):
+        pos = rng.choice(V, size=min(64, V), replace=False)
+        x[r, pos] = (1.0 - np.arange(len(pos)) * 2.0 ** -24).astype(np.float32)
+    return x
+
+
+@pytest.mark.parametrize("shape", ["auto", "split", "warp", "cta"])
+@pytest.mark.parametrize("V", [100, 5003, 70001, 300000])
+def test_safe_fused_topk_collisions_bit_exact(cuda, oracle_mod, lib, shape, V):
+    """safe_softmax_fused_topk selects on float(expf(x - m) / d) with a double
+    d (kernels.hpp:95-98): with colliding probabilities only the reference's
+    exact arithmetic reproduces its indices.  k = 5, 32 and (large-k path) 40."""
+    from paper_1805_02867_b200 import osmx
+
+    if shape in ("warp", "cta"):
+        lib.config_set("topk_threads", 32 if shape == "warp" else 256)
+    else:
+        lib.config_set("shape", SHAPES[shape])
+    rng = np.random.default_rng(V)
+    x = _collision_rows(rng, 4, V)
+    for k in (5, 32, 40):
+        if k > V:
+            continue
+        vals, idx = osmx.softmax_topk(_dev(x), k, alg="safe_fused")
+        rv, rz = _topk_ref(oracle_mod, "safe_softmax_fused_topk", x, k)
+        assert np.array_equal(idx.cpu().numpy(), rz), (k, shape)
+        assert np.array_equal(vals.cpu().numpy().view(np.int32), rv.view(np.int32)), (k, shape)
+        # the collisions are real: some selected probabilities are equal
+        assert (np.diff(rv, axis=1) == 0).any()

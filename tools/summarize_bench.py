@@ -24,7 +24,8 @@ if sw:
     for r in sw["topk"]:
         print(f"{r['V']:>8} {r['online_fused']['ms']:>9} {r['online_fused']['frac']:>6} {r['online_unfused']['ms']:>9} "
               f"{r['fused_over_online_unfused']:>6} {r['safe_unfused']['ms']:>9} {r['fused_over_safe_unfused']:>6} "
-              f"{r.get('online_unfused_stream', {}).get('ms', 0):>9} {r.get('fused_over_online_unfused_stream', 0):>6}")
+              f"{r.get('online_unfused_stream', {}).get('ms', 0):>9} {r.get('fused_over_online_unfused_stream', 0):>6}"
+              f"  safe_fused {r.get('safe_fused', {}).get('ms', 0)}")
     if "c5" in sw:
         print("c5", json.dumps(sw["c5"]))
     if "c1_parity" in sw:
