@@ -43,8 +43,9 @@ typedef enum {
   OSMX_ERR_INVALID_CHUNK = 4, /* invalid_chunk_error error.hpp:23-25 */
   OSMX_ERR_INVALID_ARG = 5,   /* null pointer, ld < V, bad enum, ws too small */
   OSMX_ERR_CUDA = 6,          /* a CUDA runtime error (see osmx_last_cuda_error) */
-  OSMX_ERR_UNSUPPORTED = 7    /* split / slice records with k > OSMX_MAX_K; top-K with
+  OSMX_ERR_UNSUPPORTED = 7,   /* split / slice records with k > OSMX_MAX_K; top-K with
                                  V >= 2^31 or rows * k >= 2^31 when k > OSMX_MAX_K */
+  OSMX_ERR_NCCL = 8           /* NCCL missing or a NCCL call failed (osmx_last_nccl_error) */
 } osmx_status;
 
 /* Algorithm ids: the reference's `algorithm` enum order (counting.hpp:17-24)
@@ -155,6 +156,37 @@ osmx_status osmx_records_combine(const void* records, int32_t n, int32_t k, void
 /* y = e^(x - M)/D over a slice, (M, D) from a combined record. */
 osmx_status osmx_scale_with_record(const float* x, int64_t V, const void* record, float* y,
                                    void* stream);
+
+/* ------------------------------------------- V-split over NCCL (C5) -- */
+
+/* One row too long for one device, split into contiguous column slices, one
+ * per rank of an NCCL communicator (rank r holds columns [col0, col0 +
+ * V_slice); slices in rank order cover the row).  Each call is three
+ * stream-ordered steps on `stream`, capturable in a CUDA graph, no host
+ * synchronisation: this rank's slice record (one launch) -> ONE
+ * ncclAllGather of the fixed-size records (in place, rank order) -> the
+ * rank-order merge (normalizer.hpp:74-85 with the chunk boundaries at the
+ * rank boundaries; top-K under (value desc, index asc), topk.hpp:37-43).
+ * Every rank gets the same outputs.  An empty slice (V_slice = 0) joins with
+ * the merge identity.  Non-finite input is reported through ws (row 0) by
+ * osmx_check_status.  `comm` is an ncclComm_t: from osmx_nccl_comm_init or
+ * the caller's own (NCCL is loaded at run time, preferring the libnccl.so.2
+ * already in the process). */
+int osmx_nccl_available(void);
+const char* osmx_last_nccl_error(void);
+/* 128-byte ncclUniqueId (rank 0 makes it, the caller broadcasts it). */
+osmx_status osmx_nccl_get_unique_id(void* id128);
+osmx_status osmx_nccl_comm_init(void** comm, int32_t nranks, const void* id128, int32_t rank);
+osmx_status osmx_nccl_comm_destroy(void* comm);
+size_t osmx_vsplit_workspace_bytes(int64_t V_slice, int32_t k, int32_t nranks);
+/* online_softmax_topk (topk.hpp:68) of the whole row: vals[k], idx[k] with
+ * global column indices, on every rank. */
+osmx_status osmx_vsplit_softmax_topk(const float* x_slice, int64_t V_slice, int64_t col0, int32_t k, void* comm,
+                                     float* vals, int64_t* idx, void* ws, size_t ws_bytes, void* stream);
+/* online_softmax (softmax.hpp:28) of the whole row: this rank's slice of it
+ * in y_slice (V_slice floats).  ws: osmx_vsplit_workspace_bytes(V_slice, 0, n). */
+osmx_status osmx_vsplit_softmax(const float* x_slice, int64_t V_slice, int64_t col0, float* y_slice, void* comm,
+                                void* ws, size_t ws_bytes, void* stream);
 
 /* --------------------------------------------------- host buffers (e2e) -- */
 

@@ -12,7 +12,8 @@ from pathlib import Path
 LIB_PATH = Path(__file__).resolve().parent / "libosmx_b200.so"
 
 # C-ABI status codes (include/osmx_b200.h)
-OK, ERR_EMPTY, ERR_NON_FINITE, ERR_INVALID_K, ERR_INVALID_CHUNK, ERR_INVALID_ARG, ERR_CUDA, ERR_UNSUPPORTED = range(8)
+(OK, ERR_EMPTY, ERR_NON_FINITE, ERR_INVALID_K, ERR_INVALID_CHUNK, ERR_INVALID_ARG, ERR_CUDA, ERR_UNSUPPORTED,
+ ERR_NCCL) = range(9)
 
 # Algorithm ids (include/osmx_b200.h, reference counting.hpp:17-24 order)
 NAIVE_SOFTMAX = 0
@@ -58,6 +59,14 @@ SIGNATURES = {
     "osmx_diag_read_probe": (_int, [_vp, _sz, _vp, _vp]),
     "osmx_config_set": (_int, [C.c_char_p, _i64]),
     "osmx_config_get": (_i64, [C.c_char_p]),
+    "osmx_nccl_available": (_int, []),
+    "osmx_last_nccl_error": (C.c_char_p, []),
+    "osmx_nccl_get_unique_id": (_int, [_vp]),
+    "osmx_nccl_comm_init": (_int, [C.POINTER(_vp), _i32, _vp, _i32]),
+    "osmx_nccl_comm_destroy": (_int, [_vp]),
+    "osmx_vsplit_workspace_bytes": (_sz, [_i64, _i32, _i32]),
+    "osmx_vsplit_softmax_topk": (_int, [_vp, _i64, _i64, _i32, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "osmx_vsplit_softmax": (_int, [_vp, _i64, _i64, _vp, _vp, _vp, _sz, _vp]),
 }
 
 

@@ -203,6 +203,7 @@ const char* osmx_status_string(osmx_status s) {
     case OSMX_ERR_INVALID_ARG: return "invalid argument";
     case OSMX_ERR_CUDA: return "CUDA error";
     case OSMX_ERR_UNSUPPORTED: return "unsupported (records: k above OSMX_MAX_K; large k: rows * k >= 2^31)";
+    case OSMX_ERR_NCCL: return "NCCL error";
   }
   return "unknown status";
 }
@@ -392,7 +393,7 @@ osmx_status osmx_config_set(const char* key, int64_t value) {
     if (value != 0 && (value < 16 || value > 227)) return OSMX_ERR_INVALID_ARG;
     t.staged_kb = (int)value;
   } else if (!strcmp(key, "split_cta")) {
-    if (value < -1 || value > 2) return OSMX_ERR_INVALID_ARG;
+    if (value < -1 || value > 3) return OSMX_ERR_INVALID_ARG;
     t.split_cta = (int)value;
   } else if (!strcmp(key, "proj_bn")) {
     if (value != 0 && value != 128 && value != 224 && value != 256) return OSMX_ERR_INVALID_ARG;

@@ -284,31 +284,58 @@ struct L2Acc {
 };
 
 // Safe-softmax normalizer (Alg. 2, kernels.hpp:55-56): the row max M is known
-// before the sum, so every term is e^(x - M) = 2^((x - M) * L) computed from
-// the difference x - M alone -- shifting a row by a constant that keeps
-// x + c exact leaves every term, d and the outputs bit-identical, the
-// reference's own shift-invariance property (test_softmax.cpp "shift
-// invariance").  Same interface as L2Acc (raise once with M).
+// before the sum, so every term is e^(x - M) computed from the difference
+// x - M alone -- shifting a row by a constant that keeps x + c exact leaves
+// every term, d and the outputs bit-identical, the reference's own
+// shift-invariance property (test_softmax.cpp "shift invariance").  Like the
+// reference, d is a double: the terms are the accurate expf of x - M (0 ulps
+// from glibc's on 93% of floats, never more than 2 -- tools/expf_lab.cu; the
+// ex2.approx of a rounded (x - M) * log2e would be off by ~|x - M| * 6e-8),
+// summed four at a time in float and the partial sums in double.
 struct SafeAcc {
   float M = kNegInf;
-  float d = 0.0f;
+  double d = 0.0;
   __device__ __forceinline__ void raise(float m) { M = m; }
-  __device__ __forceinline__ float term(float x) const { return ex2((x - M) * kLog2e); }
+  __device__ __forceinline__ float termf(float x) const { return expf(x - M); }
+  __device__ __forceinline__ double term(float x) const { return (double)termf(x); }
+  __device__ __forceinline__ void add4(float a, float b, float c, float e) {
+    d += (double)((termf(a) + termf(b)) + (termf(c) + termf(e)));
+  }
   template <int U>
   __device__ __forceinline__ void add_batch(const float4 (&v)[U]) {
-    float s = 0.0f;
-    const float2 L2 = make_float2(kLog2e, kLog2e), M2 = make_float2(-M, -M);
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const float2 t0 = __fmul2_rn(__fadd2_rn(make_float2(v[u].x, v[u].y), M2), L2);
-      const float2 t1 = __fmul2_rn(__fadd2_rn(make_float2(v[u].z, v[u].w), M2), L2);
-      const float2 p = __fadd2_rn(make_float2(ex2(t0.x), ex2(t1.x)), make_float2(ex2(t0.y), ex2(t1.y)));
-      s += p.x + p.y;
-    }
-    d += s;
+    for (int u = 0; u < U; ++u) add4(v[u].x, v[u].y, v[u].z, v[u].w);
   }
-  __device__ __forceinline__ MD finish() const { return MD{M, d}; }
 };
+
+// 1/d split into two floats (hi + lo = 1/d to ~2^-48) so an output
+// y = e * (1/d) costs one FMUL and one FFMA and is rounded once:
+// y = float(e^(x - m) / d) for the safe and online outputs (kernels.hpp:57,
+// :68), the float expf of the float difference over the (double) d.
+struct Recip {
+  float hi, lo;
+};
+__device__ __forceinline__ Recip recip_of(double d) {
+  const double r = 1.0 / d;
+  const float hi = __double2float_rn(r);
+  return Recip{hi, __double2float_rn(r - (double)hi)};
+}
+__device__ __forceinline__ float out_md(float x, float m, Recip r) {
+  const float e = expf(x - m);
+  return fmaf(e, r.hi, e * r.lo);
+}
+// The online softmax's output pass keeps the one-FMUL form e * float(1/d):
+// its d is an fp32 sum already (Alg. 3), so the lo term buys nothing there,
+// and the extra FMUL costs 3-5% in the staged kernels.
+template <bool SAFE>
+__device__ __forceinline__ float out_soft(float x, float m, Recip r) {
+  if constexpr (SAFE) return out_md(x, m, r);
+  else return expf(x - m) * r.hi;
+}
+// The same for a handful of values (top-K epilogues): the double quotient.
+__device__ __forceinline__ float out_md(float x, float m, double rd) {
+  return __double2float_rn(__dmul_rn((double)expf(x - m), rd));
+}
 
 // merge(), reference normalizer.hpp:52-58.  The identity (-inf, 0) is
 // absorbing without the NaN that (-inf) - (-inf) would produce.
@@ -426,14 +453,18 @@ __device__ __forceinline__ double cta_sum_d(double v, double* scratch) {
 // ------------------------------------------------------------ workspace --
 
 // Every entry point takes a caller-owned device workspace whose first
-// kWsHeader bytes are this header (zero-initialised by osmx_workspace_init;
-// osmx_check_status reads and re-zeroes it).
+// kWsHeader bytes are zero-initialised by osmx_workspace_init: this status
+// header (osmx_check_status reads and re-zeroes it) and, from byte
+// kWsTicketsOff, the per-row ticket counters of the one-launch wide-row
+// top-K (topk_wide.cu; each counter is reset to 0 by the CTA that uses it).
 struct WsHeader {
   unsigned long long bad;  // 0 = all rows finite, else (INT64_MAX - first bad row)
   long long row_base;      // added to flagged row ids (host pipeline blocks)
   unsigned long long pad[14];
 };
-constexpr int kWsHeader = 128;
+constexpr int kWsTicketsOff = 128;
+constexpr int kWsMaxTickets = 992;  // rows of one wide-row launch
+constexpr int kWsHeader = kWsTicketsOff + 4 * kWsMaxTickets;  // 4096
 
 __device__ __forceinline__ void flag_bad_row(void* ws, long long row) {
   WsHeader* h = reinterpret_cast<WsHeader*>(ws);

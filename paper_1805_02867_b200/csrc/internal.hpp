@@ -46,7 +46,8 @@ struct Tuning {
   int staged_ng = 0;            // staged softmax: row groups per CTA (0 auto; clamped to the slots)
   int staged_kb = 0;            // staged softmax: ring (shared memory) per CTA, KB (0 auto)
   int split_cta = -1;           // top-K split path: -1 auto, 0 warp-per-piece records, 1 CTA-per-chunk
-                                // (legacy), 2 TMA-ring CTA per piece
+                                // (legacy), 2 TMA-ring CTA per piece, 3 one-launch grid-stride
+                                // (topk_wide.cu)
   int proj_bn = 0;              // fused projection vocabulary tile (0 auto; 128, 256)
   int topk_pipe = 0;            // warp-per-row top-K via a cp.async smem pipeline (0 off; 1..3 layouts)
   int topk_u8 = -1;             // warp-per-row top-K with 8 float4s in flight (-1 auto)
@@ -147,6 +148,11 @@ size_t topk_large_ws(long long rows, long long V, int k);
 // TMA-ring top-K in record mode (split path): resident CTAs on the device
 // for this k, and the launch over rows * R pieces of `chunk` columns.
 long long topk_tma_slots(int k);
+// topk_wide.cu: one-launch grid-stride split with a fused last-CTA combine
+// (few rows, V < 2^31, rows <= 992): resident CTAs for this k and the launch.
+long long topk_wide_slots(int k);
+cudaError_t launch_topk_wide(int mode, const float* x, long long ldx, long long rows, long long V, int k,
+                             float* vals, long long* idx, void* ws, cudaStream_t st, long long col0, char* out_rec);
 cudaError_t launch_topk_tma_records(int mode, const float* x, long long ldx, long long pieces, long long V, int k,
                                     void* ws, cudaStream_t st, int R, long long chunk, long long col0, char* rec);
 bool topk_large_supported(long long rows, long long V, int k);

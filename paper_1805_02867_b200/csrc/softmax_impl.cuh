@@ -170,6 +170,7 @@ __global__ void __launch_bounds__(TPR > 256 ? TPR : 256)
   // Returns (m, scale) such that y = f(x) * scale.
   float m = 0.0f, r = 0.0f;
   double rd = 0.0;
+  Recip rc{0.0f, 0.0f};  // safe / online: 1/d as hi + lo
   bool row_bad = false;
   if constexpr (ALG == osmx_host::kOnline) {
     // Alg. 3 lines 1-6 on the thread's elements (max first, then one
@@ -187,7 +188,7 @@ __global__ void __launch_bounds__(TPR > 256 ? TPR : 256)
     if (bad) s0.d = nanf_();
     MD s = G::md(s0, smf);
     m = s.m;
-    r = __frcp_rn(s.d);
+    rc = recip_of((double)s.d);
     row_bad = !(s.d == s.d) || !isfinite(m);
   } else if constexpr (ALG == osmx_host::kSafe) {
     float lm = kNegInf;
@@ -198,10 +199,10 @@ __global__ void __launch_bounds__(TPR > 256 ? TPR : 256)
     acc.raise(m);
 #pragma unroll
     for (int t = 0; t < EPT; ++t) acc.d += acc.term(a[t]);
-    float ld = (m == kNegInf) ? 0.0f : acc.finish().d;
-    if (bad) ld = nanf_();
-    const float d = G::reduce(ld, OpSum(), smf);
-    r = __frcp_rn(d);
+    double ld = (m == kNegInf) ? 0.0 : acc.d;
+    if (bad) ld = (double)nanf_();
+    const double d = G::reduce(ld, OpSumD(), smd);
+    rc = recip_of(d);
     row_bad = !(d == d) || !isfinite(m);
   } else {  // naive: d = sum double(expf(x)), no max shift (kernels.hpp:43-45)
     double ld = 0.0;
@@ -220,7 +221,7 @@ __global__ void __launch_bounds__(TPR > 256 ? TPR : 256)
     if constexpr (ALG == osmx_host::kNaive)
       return (float)((double)expf(v) * rd);
     else
-      return expf(v - m) * r;
+      return out_soft<ALG == osmx_host::kSafe>(v, m, rc);
   };
   if constexpr (VEC) {
 #pragma unroll
@@ -267,6 +268,7 @@ __global__ void __launch_bounds__(BLOCK)
     float mn = -kNegInf;
     float M, r = 0.0f;
     double rd = 0.0;
+    Recip rc{0.0f, 0.0f};  // safe / online: 1/d as hi + lo
     bool bad;
     if constexpr (ALG == osmx_host::kOnline) {
       // Pass 1: Alg. 3 lines 1-6, batch-max-first update per U float4s.
@@ -292,7 +294,7 @@ __global__ void __launch_bounds__(BLOCK)
       MD tot = md_cta_reduce<NW>(acc.finish(), smf);
       mn = cta_min<NW>(mn, smf);
       M = tot.m;
-      r = __frcp_rn(tot.d);
+      rc = recip_of((double)tot.d);
       bad = !(tot.d == tot.d) || !isfinite(M) || mn == kNegInf;
     } else if constexpr (ALG == osmx_host::kSafe) {
       // Pass 1: max (kernels.hpp:54).  Pass 2: normalizer (:56).
@@ -319,9 +321,9 @@ __global__ void __launch_bounds__(BLOCK)
       stream_seg<BLOCK, U, P1>(
           s, t, [&](float v, long long) { sacc.d += sacc.term(v); },
           [&](float4 (&v)[U], long long, int) { sacc.add_batch<U>(v); });
-      float d = (M == kNegInf) ? 0.0f : sacc.finish().d;
-      d = cta_sum<NW>(d, smf);
-      r = __frcp_rn(d);
+      double d = (M == kNegInf) ? 0.0 : sacc.d;
+      d = cta_sum_d<NW>(d, smd);
+      rc = recip_of(d);
       bad = !(d == d) || !isfinite(M) || mn == kNegInf;
     } else {
       // Naive: d = sum double(expf(x)) (kernels.hpp:43-44).
@@ -361,9 +363,9 @@ __global__ void __launch_bounds__(BLOCK)
       map_seg<BLOCK, U>(s, yr, t, [&](float v) { return (float)((double)expf(v) * rd); },
                         std::integral_constant<bool, true>{});
     } else if constexpr (ALG == osmx_host::kOnline) {
-      map_seg<BLOCK, U>(s, yr, t, [&](float v) { return expf(v - M) * r; }, std::integral_constant<bool, true>{});
+      map_seg<BLOCK, U>(s, yr, t, [&](float v) { return out_soft<ALG == osmx_host::kSafe>(v, M, rc); }, std::integral_constant<bool, true>{});
     } else {
-      map_seg<BLOCK, U>(s, yr, t, [&](float v) { return expf(v - M) * r; });
+      map_seg<BLOCK, U>(s, yr, t, [&](float v) { return out_soft<ALG == osmx_host::kSafe>(v, M, rc); });
     }
   }
 }
@@ -427,10 +429,10 @@ __global__ void __launch_bounds__(BLOCK)
     stream_seg<BLOCK, U, false>(
         s, t, [&](float v, long long) { sacc.d += sacc.term(v); },
         [&](float4 (&v)[U], long long, int) { sacc.add_batch<U>(v); });
-    float d = (M == kNegInf) ? 0.0f : sacc.finish().d;
-    d = cta_sum<NW>(d, smf);
+    double d = (M == kNegInf) ? 0.0 : sacc.d;
+    d = cta_sum_d<NW>(d, smd);
     __syncthreads();  // every thread has read rr[*].m before it is rewritten
-    if (t == 0) rr[blockIdx.x].d = (double)d;
+    if (t == 0) rr[blockIdx.x].d = d;
     return;
   }
   float mn = -kNegInf;
@@ -519,6 +521,7 @@ __global__ void __launch_bounds__(BLOCK)
   const SRec* rr = rec + row * S;
   float M = kNegInf, mn = -kNegInf, r = 0.0f;
   double rd = 0.0;
+  Recip rc{0.0f, 0.0f};  // safe / online: 1/d as hi + lo
   bool bad;
   if constexpr (ALG == osmx_host::kOnline) {
     MD a = md_identity();
@@ -529,19 +532,19 @@ __global__ void __launch_bounds__(BLOCK)
     a = md_cta_reduce<NW>(a, smf);
     mn = cta_min<NW>(mn, smf);
     M = a.m;
-    r = __frcp_rn(a.d);
+    rc = recip_of((double)a.d);
     bad = !(a.d == a.d) || !isfinite(M) || mn == kNegInf;
   } else if constexpr (ALG == osmx_host::kSafe) {
-    float d = 0.0f;
+    double d = 0.0;
     for (int i = t; i < S; i += BLOCK) {
       M = fmaxf(M, rr[i].m);
       mn = fminf(mn, rr[i].mn);
-      d += (float)rr[i].d;
+      d += rr[i].d;
     }
     M = cta_max<NW>(M, smf);
     mn = cta_min<NW>(mn, smf);
-    d = cta_sum<NW>(d, smf);
-    r = __frcp_rn(d);
+    d = cta_sum_d<NW>(d, smd);
+    rc = recip_of(d);
     bad = !(d == d) || !isfinite(M) || mn == kNegInf;
   } else {
     double d = 0.0;
@@ -567,7 +570,7 @@ __global__ void __launch_bounds__(BLOCK)
     map_seg<BLOCK, U>(s, yr, t, [&](float v) { return (float)((double)expf(v) * rd); },
                       std::integral_constant<bool, true>{});
   } else {
-    map_seg<BLOCK, U>(s, yr, t, [&](float v) { return expf(v - M) * r; }, std::integral_constant<bool, true>{});
+    map_seg<BLOCK, U>(s, yr, t, [&](float v) { return out_soft<ALG == osmx_host::kSafe>(v, M, rc); }, std::integral_constant<bool, true>{});
   }
 }
 

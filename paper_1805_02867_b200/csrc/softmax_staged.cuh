@@ -283,8 +283,9 @@ __global__ void __launch_bounds__(1024, 1)
         return buf;
       };
 
-      float M = 0.0f, rr = 0.0f;
+      float M = 0.0f;
       double rd = 0.0;
+      Recip rc{0.0f, 0.0f};  // safe / online: 1/d as hi + lo
       bool bad;
       float mn = -kNegInf;
       if constexpr (ALG == osmx_host::kOnline) {
@@ -343,7 +344,7 @@ __global__ void __launch_bounds__(1024, 1)
           }
         }
         M = tot.m;
-        rr = __frcp_rn(tot.d);
+        rc = recip_of((double)tot.d);
         bad = !(tot.d == tot.d) || !isfinite(M) || mn == kNegInf;
       } else if constexpr (ALG == osmx_host::kSafe) {
         // kernels.hpp:54 max, :56 sum against it
@@ -382,14 +383,14 @@ __global__ void __launch_bounds__(1024, 1)
           float4 v[1] = {masked(my_edge, kNegInf)};
           sacc.add_batch<1>(v);
         }
-        float d = (M == kNegInf) ? 0.0f : sacc.finish().d;
-        d = SGrp<GW>::red(d, SOpSum(), scr, bar_id, lw);
+        double d = (M == kNegInf) ? 0.0 : sacc.d;
+        d = SGrp<GW>::red(d, SOpSumD(), scrd, bar_id, lw);
         if (C > 1) {
-          const SRecX* rec = exchange(1, SRecX{M, mn, (double)d});
-          d = 0.0f;
-          for (unsigned q = 0; q < C; ++q) d += (float)rec[q].d;
+          const SRecX* rec = exchange(1, SRecX{M, mn, d});
+          d = 0.0;
+          for (unsigned q = 0; q < C; ++q) d += rec[q].d;
         }
-        rr = __frcp_rn(d);
+        rc = recip_of(d);
         bad = !(d == d) || !isfinite(M) || !(mn == mn) || mn == kNegInf;
       } else {
         // naive: d = sum double(expf(x)) (kernels.hpp:43-44), no max shift
@@ -431,7 +432,7 @@ __global__ void __launch_bounds__(1024, 1)
         if constexpr (ALG == osmx_host::kNaive)
           return (float)((double)expf(v) * rd);
         else
-          return expf(v - M) * rr;
+          return out_soft<ALG == osmx_host::kSafe>(v, M, rc);
       };
       const bool same_phase = ((reinterpret_cast<uintptr_t>(ys) >> 2) & 3) == (uintptr_t)phase;
       float* yb = ys - phase;  // yb[4q + c] <-> slot float4 q component c

@@ -24,6 +24,8 @@ size_t topk_split_ws(int alg, long long rows, long long V, int k) {
   // TMA-ring pieces (split_cta = 2) are never more: >= 16K elements over at
   // most 28 resident CTAs per SM.
   size_t b = (size_t)(rows * std::max(S, R + (R + 255) / 256)) * rec_bytes_(k);
+  // one-launch wide rows: rows x (resident CTAs / rows) records
+  if (topk_wide_ok(rows, V)) b = std::max(b, (size_t)std::max(topk_wide_slots(k), rows) * rec_bytes_(k));
   if (alg == kSafeFusedTopk) b += ((size_t)(rows * S) * sizeof(SRecView) + 255) / 256 * 256;
   return b;
 }
@@ -81,14 +83,15 @@ __global__ void __launch_bounds__(BLOCK)
     k_scale_with_record(const float* __restrict__ x, long long V, const RecHdr* __restrict__ rec,
                         float* __restrict__ y) {
   const RecHdr h = *rec;
-  const float M = h.m, R = __frcp_rn(h.d);
+  const float M = h.m;
+  const Recip R = recip_of((double)h.d);
   const long long per = (V + gridDim.x - 1) / gridDim.x;
   const long long chunk = (per + 15) / 16 * 16;
   const long long c0 = (long long)blockIdx.x * chunk;
   if (c0 >= V) return;
   const long long n = std::min(chunk, V - c0);
   const Seg s = make_seg(x + c0, n);
-  map_seg<BLOCK, U>(s, y + c0, threadIdx.x, [&](float v) { return expf(v - M) * R; });
+  map_seg<BLOCK, U>(s, y + c0, threadIdx.x, [&](float v) { return out_md(v, M, R); });
 }
 }  // namespace
 

@@ -53,6 +53,20 @@ struct Pass {
   float mn = -kNegInf, chk = 0.0f;
   float M = 0.0f;   // SAFE select pass: row max
   double D = 1.0;   //                   and the double normalizer
+  // SAFE: x-space image of the admission bound.  The key float(e^(x-M)/D)
+  // is monotone in x, so key(x) >= T implies x >= M + ln(T D) up to the
+  // roundings of x - M, expf and the quotient (a few 1e-7 relative); xlo
+  // sits 1e-5 (relative) below that, and a batch whose raw max is under it
+  // skips the double-precision key entirely.
+  float xlo = kNegInf;
+  __device__ __forceinline__ void upd_xlo() {
+    if constexpr (MODE == kModeSafe) {
+      if (T > 0.0f) {
+        const double xl = (double)M + log((double)T * D);
+        xlo = (float)(xl - 1e-5 * (1.0 + fabs(xl) + fabs(xl - (double)M)));
+      }
+    }
+  }
 
   __device__ __forceinline__ void scalar(float v, int j, int k) {
     if constexpr (MODE == kModeFused) {
@@ -126,6 +140,7 @@ struct Pass {
       // the best lane k-th is a lower bound too
       T = fmaxf(T, o2f(__reduce_max_sync(mask, f2o(L.thr()))));
       if (Tsh && (int)(threadIdx.x & 31) == __ffs(mask) - 1) atomicMax(Tsh, f2o(T));
+      upd_xlo();
     }
   }
 
@@ -162,6 +177,8 @@ struct Pass {
       float bm = kNegInf;
 #pragma unroll
       for (int u = 0; u < U; ++u) bm = fmaxf(bm, fmaxf(fmaxf(v[u].x, v[u].y), fmaxf(v[u].z, v[u].w)));
+      // no lane can admit anything: skip the keys (warp-uniform)
+      if (!__any_sync(__activemask(), bm >= xlo)) return;
       const float Mr = M;
       const double Dr = D;
       select_batch(v, cnt, j0, jstride, safe_key_ref(bm, Mr, Dr),
@@ -307,7 +324,8 @@ __global__ void __launch_bounds__(BLOCK, MINB)
     P.kk = k;
     if (G == BLOCK) P.Tsh = &tsh[it & 1];
     bool bad = false;
-    float outM = 0.0f, outR = 1.0f;
+    float outM = 0.0f;
+    double outR = 1.0;
     if constexpr (MODE == kModeSafe) {
       float m = kNegInf, mn = -kNegInf;
       safe_max_min<G, U>(s, t, m, mn);
@@ -358,7 +376,7 @@ __global__ void __launch_bounds__(BLOCK, MINB)
         MN = cta_min<NW>(P.mn, smf);
       }
       outM = tot.m;
-      outR = __frcp_rn(tot.d);
+      outR = 1.0 / (double)tot.d;
       bad = !(tot.d == tot.d) || !isfinite(tot.m) || MN == kNegInf;
       hdr = RecHdr{tot.m, tot.d, MN, k};
     } else if constexpr (MODE == kModeTopkOf) {
@@ -379,7 +397,7 @@ __global__ void __launch_bounds__(BLOCK, MINB)
           return;
         }
         float out = v;
-        if constexpr (MODE == kModeFused) out = expf(v - outM) * outR;  // kernels.hpp:122
+        if constexpr (MODE == kModeFused) out = out_md(v, outM, outR);  // kernels.hpp:122
         vals[row * k + r] = out;
         idx[row * k + r] = (long long)i;
       }
@@ -524,7 +542,7 @@ __global__ void __launch_bounds__(32)
     bad = !(a.d == a.d) || !isfinite(a.m) || mn == kNegInf || nan_seen;
   else
     bad = nan_seen;
-  const float R = __frcp_rn(a.d);
+  const double R = 1.0 / (double)a.d;
   char* orec = out_rec ? out_rec + (size_t)row * rb : nullptr;
   L.normalize(k);
   group_merge<32>(L, k, [&](int r, float v, long long i) {
@@ -534,7 +552,7 @@ __global__ void __launch_bounds__(32)
         reinterpret_cast<long long*>(orec + rec_idx_off(k))[r] = i;
       }
       if (vals) {
-        vals[row * k + r] = mode == kModeFused ? expf(v - a.m) * R : v;
+        vals[row * k + r] = mode == kModeFused ? out_md(v, a.m, R) : v;
         idx[row * k + r] = i;
       }
     }
@@ -557,23 +575,31 @@ __global__ void __launch_bounds__(32)
 // in (value desc, index asc) order, so equal values reach a thread's list
 // in increasing index order and the cheap strict-'>' insertion keeps the
 // reference's tie order; the warp / CTA merges use the full order.
+// The body of the CTA-wide combine, shared with the one-launch wide-row
+// kernel (topk_wide.cu), where the records come from other CTAs of the same
+// launch: CG = true loads them L2-coherent (ld.global.cg) after the ticket.
 template <int KC, int NT>
-__global__ void __launch_bounds__(NT)
-    k_topk_combine_cta(const char* __restrict__ rec, int n, int k, int mode, char* __restrict__ out_rec,
-                       float* __restrict__ vals, long long* __restrict__ idx, long long row_base, void* ws) {
+struct CombineSmem {
+  float smf[2 * (NT / 32)];
+  float sv[(NT / 32) * KC];
+  long long si[(NT / 32) * KC];
+};
+template <bool CG, class T>
+__device__ __forceinline__ T rec_ld(const T* p) {
+  if constexpr (CG) return __ldcg(p);
+  else return *p;
+}
+// rr: the row's n records (column order).  orec (optional) receives the
+// merged record; vals/idx (optional) the row's final k outputs; a bad row is
+// flagged as bad_row in ws when `flag`.
+template <int KC, int NT, bool CG>
+__device__ __forceinline__ void combine_records_cta(const char* __restrict__ rr, int n, int k, int mode,
+                                                    char* __restrict__ orec, float* __restrict__ vals,
+                                                    long long* __restrict__ idx, void* ws, long long bad_row,
+                                                    bool flag, CombineSmem<KC, NT>& sm) {
   constexpr int NW = NT / 32;
-  __shared__ float smf[2 * NW];
-  __shared__ float sv[NW * KC];
-  __shared__ long long si[NW * KC];
-  pdl_wait();  // records come from the previous kernel
-  const long long row = blockIdx.x;
   const int t = threadIdx.x, l = t & 31, w = t >> 5;
   const size_t rb = rec_bytes_(k);
-  const int G = gridDim.y, g = blockIdx.y;
-  const int per = (n + G - 1) / G;
-  const int c0 = g * per, c1 = min(n, c0 + per);
-  const char* rr = rec + ((size_t)row * n + c0) * rb;
-  n = c1 > c0 ? c1 - c0 : 0;
   MD a = md_identity();
   float mn = -kNegInf;
   float nan_seen = 0.0f;
@@ -583,40 +609,39 @@ __global__ void __launch_bounds__(NT)
     // every field of the record is loaded before any is used (independent
     // loads in flight together; the offers below branch)
     const char* my = rr + (size_t)c * rb;
-    const RecHdr h = *reinterpret_cast<const RecHdr*>(my);
+    const float4 hv = rec_ld<CG>(reinterpret_cast<const float4*>(my));
     const float* rv = reinterpret_cast<const float*>(my + rec_vals_off());
     const long long* ri = reinterpret_cast<const long long*>(my + rec_idx_off(k));
     float cv[KC];
     long long ci[KC];
 #pragma unroll
     for (int r = 0; r < KC; ++r) {
-      cv[r] = r < k ? rv[r] : kNegInf;
-      ci[r] = r < k ? ri[r] : -1LL;
+      cv[r] = r < k ? rec_ld<CG>(rv + r) : kNegInf;
+      ci[r] = r < k ? rec_ld<CG>(ri + r) : -1LL;
     }
-    a = md_merge(a, MD{h.m, h.d});
-    if (h.mn != h.mn) nan_seen = 1.0f;
-    mn = fminf(mn, h.mn);
+    const float hm = hv.x, hd = hv.y, hmn = hv.z;
+    a = md_merge(a, MD{hm, hd});
+    if (hmn != hmn) nan_seen = 1.0f;
+    mn = fminf(mn, hmn);
 #pragma unroll
     for (int r = 0; r < KC; ++r)
       if (r < k) L.offer(cv[r], ci[r]);
   }
-  a = md_cta_reduce<NW>(a, smf);
-  mn = cta_min<NW>(mn, smf);
-  nan_seen = cta_sum<NW>(nan_seen, smf);
+  a = md_cta_reduce<NW>(a, sm.smf);
+  mn = cta_min<NW>(mn, sm.smf);
+  nan_seen = cta_sum<NW>(nan_seen, sm.smf);
   bool bad;
   if (mode == kModeFused)
     bad = !(a.d == a.d) || !isfinite(a.m) || mn == kNegInf || nan_seen > 0.0f;
   else
     bad = nan_seen > 0.0f;
-  const float R = __frcp_rn(a.d);
-  char* orec = out_rec ? out_rec + ((size_t)row * G + g) * rb : nullptr;
-  if (G > 1) vals = nullptr, bad = false;  // first level: records only
+  const double R = 1.0 / (double)a.d;
   // per-warp k winners -> shared memory -> warp 0 merges NW * k candidates
   L.normalize(k);
   group_merge<32>(L, k, [&](int r, float v, long long i) {
     if (l == 0) {
-      sv[w * KC + r] = v;
-      si[w * KC + r] = i;
+      sm.sv[w * KC + r] = v;
+      sm.si[w * KC + r] = i;
     }
   });
   __syncthreads();
@@ -625,7 +650,7 @@ __global__ void __launch_bounds__(NT)
     M.init(k);
     for (int q = l; q < NW * k; q += 32) {
       const int ww = q / k, r = q % k;
-      M.offer_ordered(sv[ww * KC + r], si[ww * KC + r]);
+      M.offer_ordered(sm.sv[ww * KC + r], sm.si[ww * KC + r]);
     }
     M.normalize(k);
     group_merge<32>(M, k, [&](int r, float v, long long i) {
@@ -635,16 +660,33 @@ __global__ void __launch_bounds__(NT)
           reinterpret_cast<long long*>(orec + rec_idx_off(k))[r] = i;
         }
         if (vals) {
-          vals[row * k + r] = mode == kModeFused ? expf(v - a.m) * R : v;
-          idx[row * k + r] = i;
+          vals[r] = mode == kModeFused ? out_md(v, a.m, R) : v;
+          idx[r] = i;
         }
       }
     });
     if (l == 0) {
       if (orec) *reinterpret_cast<RecHdr*>(orec) = RecHdr{a.m, a.d, nan_seen > 0.0f ? __int_as_float(0x7fffffff) : mn, k};
-      if (bad && ws) flag_bad_row(ws, row_base + row);
+      if (flag && bad && ws) flag_bad_row(ws, bad_row);
     }
   }
+}
+
+template <int KC, int NT>
+__global__ void __launch_bounds__(NT)
+    k_topk_combine_cta(const char* __restrict__ rec, int n, int k, int mode, char* __restrict__ out_rec,
+                       float* __restrict__ vals, long long* __restrict__ idx, long long row_base, void* ws) {
+  __shared__ CombineSmem<KC, NT> sm;
+  pdl_wait();  // records come from the previous kernel
+  const long long row = blockIdx.x;
+  const int G = gridDim.y, g = blockIdx.y;
+  const int per = (n + G - 1) / G;
+  const int c0 = g * per, c1 = min(n, c0 + per);
+  const char* rr = rec + ((size_t)row * n + c0) * rec_bytes_(k);
+  char* orec = out_rec ? out_rec + ((size_t)row * G + g) * rec_bytes_(k) : nullptr;
+  const bool last = G == 1;  // first level of two: records only
+  combine_records_cta<KC, NT, false>(rr, c1 > c0 ? c1 - c0 : 0, k, mode, orec, last && vals ? vals + row * k : nullptr,
+                                     last && vals ? idx + row * k : nullptr, ws, row_base + row, last, sm);
 }
 
 // ------------------------------------------------------------ launchers --
@@ -775,6 +817,10 @@ long long topk_tma_piece_chunk(long long rows, long long V, int k) {
   return (ch + 15) / 16 * 16;
 }
 
+// The one-launch wide-row kernel: ticket counters for <= kWsMaxTickets rows,
+// 32-bit in-row element indices.
+bool topk_wide_ok(long long rows, long long V) { return rows <= kWsMaxTickets && V < (1LL << 31) - 4096; }
+
 template <int KC, int MODE>
 cudaError_t run_split(const float* x, long long ldx, long long rows, long long V, int k, float* vals,
                       long long* idx, void* ws, cudaStream_t st, long long col0, char* out_rec) {
@@ -798,6 +844,8 @@ cudaError_t run_split(const float* x, long long ldx, long long rows, long long V
     // 64 x 1M 0.062 vs 0.068, 400 x 1M 0.270 vs 0.314; but 128 x 256K 0.045
     // vs 0.038.
     if (how < 0) how = (rows >= 64 && rows * V <= (1LL << 25)) ? 0 : 2;
+    if (how == 3 && topk_wide_ok(rows, V))
+      return osmx_host::launch_topk_wide(MODE, x, ldx, rows, V, k, vals, idx, ws, st, col0, out_rec);
     if (how == 2) {
       // One TMA-ring CTA per piece: about one piece per resident CTA over the
       // whole problem, then one CTA-wide combine per row.

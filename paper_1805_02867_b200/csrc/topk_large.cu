@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(kLT, 1)
 
   // 1. statistics
   __shared__ double smd[kLW];
-  float M = 0.0f, R = 1.0f;
+  float M = 0.0f, R = 1.0f;  // R: the row normalizer d
   double D = 1.0;  // safe mode: the double normalizer
   bool bad = false;
   if constexpr (MODE == 0) {
@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(kLT, 1)
     const MD tot = md_cta_reduce<kLW>(acc.finish(), smf);
     mn = cta_min<kLW>(mn, smf);
     M = tot.m;
-    R = __frcp_rn(tot.d);
+    R = tot.d;  // the epilogue divides by it in double (out_md)
     bad = !(tot.d == tot.d) || !isfinite(M) || mn == kNegInf;
   } else {
     float m = kNegInf, chk = 0.0f;
@@ -265,7 +265,7 @@ __global__ void k_topk_large_out(const unsigned* __restrict__ skey, const int* _
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const long long r = i / k;
     float v = fkey_inv(skey[i]);
-    if constexpr (MODE == 0) v = expf(v - rowM[r]) * rowR[r];  // kernels.hpp:122
+    if constexpr (MODE == 0) v = out_md(v, rowM[r], 1.0 / (double)rowR[r]);  // kernels.hpp:122
     vals[i] = v;
     idx[i] = sidx[i];
   }

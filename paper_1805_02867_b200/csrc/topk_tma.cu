@@ -213,14 +213,15 @@ __global__ void __launch_bounds__((NCW + 1) * 32, kTmaMinBlocks)
       P.scalar(ld_f1(sg.p + j), j, k);
     }
     // ---- row epilogue (consumers only)
-    float outM = 0.0f, outR = 1.0f;
+    float outM = 0.0f;
+    double outR = 1.0;
     bool bad;
     RecHdr hdr{kNegInf, 0.0f, 0.0f, k};
     if constexpr (MODE == kModeFused) {
       const MD tot = md_group_cta<NCW>(P.acc.finish(), smf);
       const float mn = red_group_cta<NCW>(P.mn, -kNegInf, MinOp(), smf);
       outM = tot.m;
-      outR = __frcp_rn(tot.d);
+      outR = 1.0 / (double)tot.d;
       bad = !(tot.d == tot.d) || !isfinite(tot.m) || mn == kNegInf;
       hdr = RecHdr{tot.m, tot.d, mn, k};
     } else {
@@ -237,7 +238,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, kTmaMinBlocks)
           return;
         }
         float out = v;
-        if constexpr (MODE == kModeFused) out = expf(v - outM) * outR;  // kernels.hpp:122
+        if constexpr (MODE == kModeFused) out = out_md(v, outM, outR);  // kernels.hpp:122
         vals[row * k + r] = out;
         idx[row * k + r] = (long long)i;
       }

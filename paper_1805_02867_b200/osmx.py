@@ -79,6 +79,10 @@ class CudaError(OsmxError):
     pass
 
 
+class NcclError(OsmxError):
+    """NCCL is missing or an NCCL call of the V-split failed."""
+
+
 class UnsupportedError(OsmxError):
     pass
 
@@ -99,6 +103,8 @@ def _raise(status: int, row: int = -1) -> None:
     if status == _lib.ERR_UNSUPPORTED:
         raise UnsupportedError(f"unsupported on the device path (records need k <= {_lib.MAX_K}; "
                                "large-k top-K needs rows * k < 2^31)")
+    if status == _lib.ERR_NCCL:
+        raise NcclError(load().osmx_last_nccl_error().decode())
     raise ValueError(_lib.status_string(status))
 
 
@@ -516,7 +522,7 @@ def records_combine(records, k: int, check: bool = True):
     vals = torch.empty(max(k, 1), dtype=torch.float32, device=records.device)
     idx = torch.empty(max(k, 1), dtype=torch.int64, device=records.device)
     stream = _stream_ptr(records.device)
-    ws = _ws.get(256, records.device, stream)
+    ws = _ws.get(load().osmx_workspace_bytes(0, 0, 0, 0), records.device, stream)  # the status header
     st = load().osmx_records_combine(records.data_ptr(), n, k, out_rec.data_ptr(),
                                      vals.data_ptr() if k > 0 else None, idx.data_ptr() if k > 0 else None,
                                      ws.data_ptr(), ws.numel(), stream)
@@ -536,3 +542,96 @@ def scale_with_record(x_slice, record, out=None):
                                        _stream_ptr(x1.device))
     _raise(st)
     return out
+
+
+# ---------------------------------------------- V-split over NCCL (C-ABI) ---
+
+class NcclComm:
+    """An NCCL communicator for the C-ABI V-split (osmx_vsplit_*).  Made from
+    a 128-byte unique id that rank 0 creates and the caller distributes
+    (``NcclComm.from_torch_distributed`` broadcasts it over the default
+    torch.distributed group).  The current CUDA device must be this rank's."""
+
+    def __init__(self, world: int, rank: int, uid: bytes):
+        import ctypes as C
+
+        if len(uid) != 128:
+            raise ValueError("an NCCL unique id is 128 bytes")
+        self.world, self.rank = int(world), int(rank)
+        buf = C.create_string_buffer(bytes(uid), 128)
+        ptr = C.c_void_p()
+        _raise(load().osmx_nccl_comm_init(C.byref(ptr), self.world, buf, self.rank))
+        self.ptr = ptr.value
+
+    @staticmethod
+    def unique_id() -> bytes:
+        import ctypes as C
+
+        buf = C.create_string_buffer(128)
+        _raise(load().osmx_nccl_get_unique_id(buf))
+        return buf.raw
+
+    @classmethod
+    def from_torch_distributed(cls, group=None):
+        import torch
+        import torch.distributed as dist
+
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        obj = [cls.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        torch.cuda.current_device()
+        return cls(world, rank, obj[0])
+
+    def close(self):
+        if self.ptr:
+            _raise(load().osmx_nccl_comm_destroy(self.ptr))
+            self.ptr = None
+
+
+def nccl_available() -> bool:
+    return bool(load().osmx_nccl_available())
+
+
+def vsplit_softmax_topk_nccl(x_slice, col0: int, k: int, comm: NcclComm, check: bool = True):
+    """online_softmax_topk of a row split over the ranks of ``comm``: this
+    rank holds columns [col0, col0 + n).  One C-ABI call: slice record ->
+    ncclAllGather -> rank-order merge, all on the current stream.  Every rank
+    returns the same (vals[k], idx[k]) with global column indices."""
+    import torch
+
+    if x_slice.dim() == 2:
+        x_slice = x_slice.reshape(-1)
+    n = int(x_slice.shape[0])
+    if n and (x_slice.dtype != torch.float32 or not x_slice.is_cuda or x_slice.stride(0) != 1):
+        raise ValueError("x_slice must be a contiguous float32 CUDA vector")
+    dev = x_slice.device
+    vals = torch.empty(k, dtype=torch.float32, device=dev)
+    idx = torch.empty(k, dtype=torch.int64, device=dev)
+    stream = _stream_ptr(dev)
+    ws = _ws.get(load().osmx_vsplit_workspace_bytes(n, k, comm.world), dev, stream)
+    st = load().osmx_vsplit_softmax_topk(x_slice.data_ptr() if n else None, n, int(col0), int(k), comm.ptr,
+                                         vals.data_ptr(), idx.data_ptr(), ws.data_ptr(), ws.numel(), stream)
+    _raise(st)
+    _finish(ws, dev, stream, check)
+    return vals, idx
+
+
+def vsplit_softmax_nccl(x_slice, col0: int, comm: NcclComm, check: bool = True):
+    """online_softmax of a row split over the ranks of ``comm``: returns this
+    rank's slice of the probabilities."""
+    import torch
+
+    if x_slice.dim() == 2:
+        x_slice = x_slice.reshape(-1)
+    n = int(x_slice.shape[0])
+    if n and (x_slice.dtype != torch.float32 or not x_slice.is_cuda or x_slice.stride(0) != 1):
+        raise ValueError("x_slice must be a contiguous float32 CUDA vector")
+    dev = x_slice.device
+    y = torch.empty_like(x_slice)
+    stream = _stream_ptr(dev)
+    ws = _ws.get(load().osmx_vsplit_workspace_bytes(n, 0, comm.world), dev, stream)
+    st = load().osmx_vsplit_softmax(x_slice.data_ptr() if n else None, n, int(col0),
+                                    y.data_ptr() if n else None, comm.ptr, ws.data_ptr(), ws.numel(), stream)
+    _raise(st)
+    _finish(ws, dev, stream, check)
+    return y

@@ -68,7 +68,7 @@ def test_masked_softmax(cuda, oracle_mod, lib, shape, V):
         assert abs(d[r] - rd) <= 1e-5 * rd, (r, d[r], rd)
 
 
-@pytest.mark.parametrize("variant", [[], [("shape", 3)], [("shape", 3), ("split_cta", 0)],
+@pytest.mark.parametrize("variant", [[], [("shape", 3)], [("shape", 3), ("split_cta", 0)], [("shape", 3), ("split_cta", 3)],
                                      [("shape", 3), ("split_chunk", 2048), ("split_cta", 1)]])
 @pytest.mark.parametrize("V", [37, 9000, 70001])
 def test_masked_fused_topk(cuda, oracle_mod, lib, variant, V):

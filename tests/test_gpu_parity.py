@@ -33,6 +33,7 @@ TOPK_VARIANTS = {
     "split_warp_auto": [("shape", 3), ("split_cta", 0)],
     "split_tma": [("shape", 3), ("split_cta", 2)],
     "split_tma_small": [("shape", 3), ("split_chunk", 2048), ("split_cta", 2)],
+    "split_wide": [("shape", 3), ("split_cta", 3)],
 }
 
 
@@ -399,7 +400,7 @@ def test_online_fused_topk_many_rows(cuda, oracle_mod, lib, variant):
         assert max_rel(vals.cpu().numpy(), rv) <= TOL
 
 
-@pytest.mark.parametrize("variant", ["auto", "split_tma", "split_warp_auto"])
+@pytest.mark.parametrize("variant", ["auto", "split_tma", "split_warp_auto", "split_wide"])
 def test_topk_split_more_rows_than_ctas(cuda, oracle_mod, lib, variant):
     """Split records with more rows than resident CTAs (auto: TMA pieces up to
     5 rows per SM, one piece per row, CTAs loop over several rows), misaligned
@@ -483,7 +484,8 @@ def _collision_rows(rng, rows, V):
     Their e^(x - m) are distinct floats just below 1, but divided by d they
     round onto a coarser grid, so several share one p and the reference's
     tie rule (lowest index first, topk.hpp:37-43) decides the order."""
-    x = (rng.standard_normal((rows, V)) * 2.0 - 6.0).astype(np.float32)
+    # background capped below the 64 planted logits, so they are the top
+    x = np.minimum(rng.standard_normal((rows, V)) * 2.0 - 6.0, -1.0).astype(np.float32)
     for r in range(rows):
         pos = rng.choice(V, size=min(64, V), replace=False)
         x[r, pos] = (1.0 - np.arange(len(pos)) * 2.0 ** -24).astype(np.float32)
@@ -511,5 +513,7 @@ def test_safe_fused_topk_collisions_bit_exact(cuda, oracle_mod, lib, shape, V):
         rv, rz = _topk_ref(oracle_mod, "safe_softmax_fused_topk", x, k)
         assert np.array_equal(idx.cpu().numpy(), rz), (k, shape)
         assert np.array_equal(vals.cpu().numpy().view(np.int32), rv.view(np.int32)), (k, shape)
-        # the collisions are real: some selected probabilities are equal
-        assert (np.diff(rv, axis=1) == 0).any()
+        # the collisions are real: some selected probabilities are equal (at
+        # V = 100 the planted values' quotients land on distinct floats)
+        if V >= 5003:
+            assert (np.diff(rv, axis=1) == 0).any()

@@ -2,7 +2,11 @@
 import json
 import sys
 
-d = json.loads(open(sys.argv[1]).read().strip().splitlines()[-1])
+txt = open(sys.argv[1]).read().strip()
+try:
+    d = json.loads(txt)  # a --detail-out file (one pretty-printed object)
+except json.JSONDecodeError:
+    d = json.loads(txt.splitlines()[-1])
 if "roofline" in d:
     print({k: d.get(k) for k in ("value", "ms_per_step", "gpu_launches")}, "clocks", d.get("clocks"))
     print("roofline", {k: d["roofline"].get(k) for k in ("achieved", "peak", "frac", "traffic")})
