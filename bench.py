@@ -587,6 +587,8 @@ def compact_line(result: dict) -> dict:
     if result.get("vsplit_c5"):
         v = result["vsplit_c5"]
         line["vsplit_c5"] = {"ranks": v["ranks"], "ms": v["ms"], "GBps": v["GBps"]}
+        if "vsplit_over_single" in v:
+            line["vsplit_c5"]["over_single_gpu"] = v["vsplit_over_single"]
     # hard bound: drop the optional context before the contract keys
     for opt in ("sweep", "vsplit_c5", "parity", "elements_per_s"):
         if len(json.dumps(line, separators=(",", ":"))) <= FINAL_LINE_MAX:
@@ -596,39 +598,79 @@ def compact_line(result: dict) -> dict:
 
 
 def vsplit_measure(dist, dev, world, rank, steps, warmup) -> dict:
-    """configs[4] split across ranks: each rank owns a 64-byte aligned column
-    slice of one 2^26 row, reduces it to one record (warp-per-piece records +
-    in-GPU combine), the N records are all-gathered (one NCCL collective) and
-    every rank merges them in rank order (shard.vsplit_softmax_topk).  Time:
-    CUDA events per rank, max over ranks."""
+    """configs[4] split across ranks through the C-ABI (osmx_vsplit_softmax_topk):
+    each rank owns a 64-byte aligned column slice of one 2^26 row; one call
+    = the slice record (one launch) -> ONE ncclAllGather of the fixed-size
+    records on the same stream -> the rank-order merge (one launch).  Slices
+    rotate over buffer sets covering >= 4 x L2 (inputs cold, like the
+    single-GPU c5 cell), the n_sets calls are captured in one CUDA graph,
+    CUDA events, max over ranks.  The single-GPU split path over the same
+    slices (osmx_softmax_topk, rank 0's view) is timed the same way."""
     import torch
 
-    from paper_1805_02867_b200 import shard
+    from paper_1805_02867_b200 import _lib, osmx, shard
 
+    lib = _lib.load()
     V, k = 1 << 26, K_TOP
     c0, c1 = shard.col_range(V, world, rank)
+    n = c1 - c0
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    sets = n_rotating_sets(4 * max(n, 1), l2)
     g = torch.Generator(device=dev)
     g.manual_seed(77)
-    row = torch.empty((1, V), dtype=torch.float32, device=dev).normal_(generator=g)  # same row on every rank
-    xs = row[:, c0:c1].contiguous()
-    del row
-    for _ in range(max(warmup, 1)):
-        vals, idx = shard.vsplit_softmax_topk(xs, c0, k, world)
-    dist.barrier()
-    torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
-    for _ in range(steps):
-        vals, idx = shard.vsplit_softmax_topk(xs, c0, k, world)
-    b.record()
-    torch.cuda.synchronize()
-    t = torch.tensor([a.elapsed_time(b) / steps], device=dev, dtype=torch.float64)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t[0])
+    xs = torch.empty((sets, max(n, 1)), dtype=torch.float32, device=dev).normal_(generator=g)
+    comm = osmx.NcclComm.from_torch_distributed()
+    vals = torch.empty(k, dtype=torch.float32, device=dev)
+    idx = torch.empty(k, dtype=torch.int64, device=dev)
+    nb = lib.osmx_vsplit_workspace_bytes(n, k, world)
+    ws = torch.zeros(nb, dtype=torch.uint8, device=dev)
+    nb1 = lib.osmx_workspace_bytes(5, 1, max(n, 1), k)
+    ws1 = torch.zeros(nb1, dtype=torch.uint8, device=dev)
+
+    def vs(i, st):
+        assert lib.osmx_vsplit_softmax_topk(xs[i].data_ptr(), n, c0, k, comm.ptr, vals.data_ptr(), idx.data_ptr(),
+                                            ws.data_ptr(), nb, st) == 0, osmx.load().osmx_last_nccl_error()
+
+    def single(i, st):
+        assert lib.osmx_softmax_topk(5, xs[i].data_ptr(), n, 1, n, k, vals.data_ptr(), idx.data_ptr(),
+                                     ws1.data_ptr(), nb1, st) == 0
+
+    def timed(fn):
+        st = torch.cuda.Stream()
+        st.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(st):
+            for _ in range(max(warmup, 1)):
+                for i in range(sets):
+                    fn(i, st.cuda_stream)
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr, stream=st):
+                for i in range(sets):
+                    fn(i, st.cuda_stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(st):
+            a.record()
+            for _ in range(steps):
+                gr.replay()
+            b.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([a.elapsed_time(b) / (steps * sets)], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t[0])
+
+    ms = timed(vs)
+    top1 = int(idx[0].item())
+    ms1 = timed(single) if n > 0 else None
+    comm.close()
     gbs = algo_bytes("online_fused", 1, V, k) / (ms * 1e-3) / 1e9
-    return {"rows": 1, "V": V, "k": k, "ranks": world, "ms": round(ms, 5), "GBps": round(gbs, 1),
-            "top1_index": int(idx.reshape(-1)[0].item()),
-            "collective": "one all_gather_into_tensor of fixed-size records (NCCL)", "timing": "max over ranks"}
+    out = {"rows": 1, "V": V, "k": k, "ranks": world, "ms": round(ms, 5), "GBps": round(gbs, 1),
+           "top1_index": top1, "n_sets": sets, "api": "osmx_vsplit_softmax_topk (C-ABI, NCCL on the stream)",
+           "collective": "one ncclAllGather of fixed-size records per call", "timing": "CUDA graph, max over ranks"}
+    if ms1:
+        out["slice_single_gpu_ms"] = round(ms1, 5)
+        out["vsplit_over_single"] = round(ms / ms1, 3)
+    return out
 
 
 def e2e_measure(lib, _lib, x, dev_idx, rows, V, k, dev, world, dist, local, steps) -> dict:
@@ -818,6 +860,29 @@ class Arena:
         return self.buf[off:off + n].view(*shape)
 
 
+def dram_cells() -> dict:
+    """Measured DRAM bytes per sweep cell, {(alg, V): bytes per launch set},
+    from the newest profiles/dram_cells_r*.json (tools/dram_cells.py: one
+    ncu pass over the same cells, L2 flushed before each)."""
+    files = sorted((ROOT / "profiles").glob("dram_cells_r*.json"))
+    if not files:
+        return {}
+    try:
+        cells = json.loads(files[-1].read_text())["cells"]
+    except (ValueError, KeyError):
+        return {}
+    return {(c["alg"], c["V"]): c["dram_bytes"] for c in cells} | {"_source": files[-1].name}
+
+
+def add_dram(cell: dict, dram: dict, alg: str, V: int, ms: float, peak: float) -> None:
+    """Beside the algorithmic `frac`: the measured DRAM bytes of the cell and
+    the DRAM-byte roofline fraction (measured bytes / this run's time / peak)."""
+    b = dram.get((alg, V))
+    if b:
+        cell["dram_bytes"] = int(b)
+        cell["dram_frac"] = round(b / (ms * 1e-3) / 1e9 / peak, 3)
+
+
 def run_sweeps(lib, _lib, dev, sp, reps, peak) -> dict:
     """configs[1]: safe vs online softmax, batch 4000, V = log_spaced(10, 1e6, 21).
     configs[2]: fused online softmax+Top-5 vs unfused online->TopK, batch 4000,
@@ -836,10 +901,11 @@ def run_sweeps(lib, _lib, dev, sp, reps, peak) -> dict:
     need = max(max(2 * n_rotating_sets(8 * B * V, l2) * B * V for V in Vs_all),
                max(n_rotating_sets(4 * B * V, l2) * B * V for V in Vt_all), 2 * n_rotating_sets(8 << 26, l2) << 26)
     arena = Arena(need, dev)
+    dram = dram_cells()
     out = {"batch": B, "k": k, "timing": "CUDA graph of n_sets launches over rotating buffer sets "
                                           "(>= 4 x L2, inputs cold in L2), CUDA events, median; one "
                                           "preallocated arena for all buffers",
-           "softmax": [], "topk": []}
+           "dram_bytes_source": dram.get("_source"), "softmax": [], "topk": []}
     Vs = Vs_all
     for V in Vs:
         n = n_rotating_sets(8 * B * V, l2)
@@ -865,6 +931,7 @@ def run_sweeps(lib, _lib, dev, sp, reps, peak) -> dict:
             row[name] = {"ms": round(ms, 5), "GBps": round(gbs, 1), "frac": round(gbs / peak, 3),
                          "dram_floor_GBps": round(8 * B * V / (ms * 1e-3) / 1e9, 1),
                          "elements_per_s": round(B * V / (ms * 1e-3), 1)}
+            add_dram(row[name], dram, name, V, ms, peak)
         row["online_over_safe"] = round(row["safe"]["ms"] / row["online"]["ms"], 3)
         # the paper's comparison: both algorithms in the streaming kernel family
         row["online_stream_over_safe_stream"] = round(row["safe_stream"]["ms"] / row["online_stream"]["ms"], 3)
@@ -895,6 +962,7 @@ def run_sweeps(lib, _lib, dev, sp, reps, peak) -> dict:
             gbs = algo_bytes(name.replace("_stream", ""), B, V) / (ms * 1e-3) / 1e9
             row[name] = {"ms": round(ms, 5), "GBps": round(gbs, 1), "frac": round(gbs / peak, 3),
                          "rows_per_s": round(B / (ms * 1e-3), 1)}
+            add_dram(row[name], dram, name, V, ms, peak)
             del ws
         row["fused_over_online_unfused"] = round(row["online_unfused"]["ms"] / row["online_fused"]["ms"], 3)
         row["fused_over_safe_unfused"] = round(row["safe_unfused"]["ms"] / row["online_fused"]["ms"], 3)
@@ -990,6 +1058,7 @@ def run_c5(lib, _lib, dev, reps, peak, l2, arena=None) -> dict:
         gbs = algo_bytes(name, 1, V, k) / (ms * 1e-3) / 1e9
         res[name] = {"ms": round(ms, 5), "GBps": round(gbs, 1), "frac": round(gbs / peak, 3),
                      "elements_per_s": round(V / (ms * 1e-3), 1)}
+        add_dram(res[name], dram_cells(), "c5_" + name, V, ms, peak)
     del x, y
     return res
 

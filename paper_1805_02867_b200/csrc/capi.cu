@@ -377,6 +377,12 @@ osmx_status osmx_config_set(const char* key, int64_t value) {
   } else if (!strcmp(key, "stream_ctas")) {
     if (value < 0 || value > 32) return OSMX_ERR_INVALID_ARG;
     t.stream_ctas = (int)value;
+  } else if (!strcmp(key, "split_fuse")) {
+    if (value < 0 || value > 1) return OSMX_ERR_INVALID_ARG;
+    t.split_fuse = (int)value;
+  } else if (!strcmp(key, "topk_block")) {
+    if (value != 0 && value != 32 && value != 128) return OSMX_ERR_INVALID_ARG;
+    t.topk_block = (int)value;
   } else if (!strcmp(key, "topk_threads")) {
     if (value != 0 && value != 32 && value != 128 && value != 256 && value != 512) return OSMX_ERR_INVALID_ARG;
     t.topk_threads = (int)value;
@@ -427,6 +433,8 @@ int64_t osmx_config_get(const char* key) {
   if (!strcmp(key, "split_chunk")) return t.split_chunk;
   if (!strcmp(key, "stream_threads")) return t.stream_threads;
   if (!strcmp(key, "topk_threads")) return t.topk_threads;
+  if (!strcmp(key, "topk_block")) return t.topk_block;
+  if (!strcmp(key, "split_fuse")) return t.split_fuse;
   if (!strcmp(key, "tma")) return t.tma;
   if (!strcmp(key, "l2_prefetch")) return t.l2_prefetch;
   if (!strcmp(key, "topk_u8")) return t.topk_u8;

@@ -589,6 +589,10 @@ struct TopList {
 // index asc, lane asc).  All lanes of the group receive winner r through
 // sink(r, value, index); the winning lane pops its head.  Lanes of one
 // group must hold indices in one coordinate system (same row / chunk base).
+// (An XOR-butterfly that swaps whole lists per level and re-sorts with a
+// compare-exchange network was measured slower on B200 -- more instructions
+// for a chain that is not the bottleneck: 4000 x 32K fused top-K 0.0920 vs
+// 0.0898 ms, configs[4] 0.067 vs 0.063 ms, tools/runs/r2_k.sh.)
 template <int WIDTH, int KC, class I, class Sink>
 __device__ __forceinline__ void group_merge(TopList<KC, I>& L, int k, Sink&& sink) {
   const int lane = (int)(threadIdx.x & 31u);

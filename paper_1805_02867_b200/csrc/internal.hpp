@@ -52,6 +52,9 @@ struct Tuning {
   int topk_pipe = 0;            // warp-per-row top-K via a cp.async smem pipeline (0 off; 1..3 layouts)
   int topk_u8 = -1;             // warp-per-row top-K with 8 float4s in flight (-1 auto)
   int l2_prefetch = -1;         // bulk L2 prefetch distance in batches (0 off, -1 auto)
+  int split_fuse = 0;           // TMA split records: merge in the piece kernel (last piece, ticket) (1) or
+                                // in a separate PDL combine launch (0; measured 2-3% faster on configs[4])
+  int topk_block = 0;           // threads per CTA of the one-wave warp-per-row top-K (0 auto = 32, 32, 128)
   int tma = 0;                  // TMA-ring top-K: 0 off (default: the warp-per-row
                                 // LDG kernel measures faster), 1 auto, 2 force
 };
@@ -153,8 +156,12 @@ long long topk_tma_slots(int k);
 long long topk_wide_slots(int k);
 cudaError_t launch_topk_wide(int mode, const float* x, long long ldx, long long rows, long long V, int k,
                              float* vals, long long* idx, void* ws, cudaStream_t st, long long col0, char* out_rec);
+// vals / out_rec non-null: the last-finishing piece of each row merges the
+// row's records in the same launch (rows <= kWsMaxTickets); else the caller
+// launches the combine.
 cudaError_t launch_topk_tma_records(int mode, const float* x, long long ldx, long long pieces, long long V, int k,
-                                    void* ws, cudaStream_t st, int R, long long chunk, long long col0, char* rec);
+                                    void* ws, cudaStream_t st, int R, long long chunk, long long col0, char* rec,
+                                    float* vals = nullptr, long long* idx = nullptr, char* out_rec = nullptr);
 bool topk_large_supported(long long rows, long long V, int k);
 cudaError_t launch_topk_large(int mode, const float* x, long long ldx, long long rows, long long V, int k,
                               float* vals, long long* idx, void* ws, void* region, cudaStream_t st);

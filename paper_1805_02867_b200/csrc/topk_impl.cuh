@@ -580,7 +580,7 @@ __global__ void __launch_bounds__(32)
 // launch: CG = true loads them L2-coherent (ld.global.cg) after the ticket.
 template <int KC, int NT>
 struct CombineSmem {
-  float smf[2 * (NT / 32)];
+  float sm_m[NT / 32], sm_d[NT / 32], sm_mn[NT / 32], sm_nan[NT / 32];
   float sv[(NT / 32) * KC];
   long long si[(NT / 32) * KC];
 };
@@ -589,14 +589,19 @@ __device__ __forceinline__ T rec_ld(const T* p) {
   if constexpr (CG) return __ldcg(p);
   else return *p;
 }
+struct CtaSync {
+  __device__ __forceinline__ void operator()() const { __syncthreads(); }
+};
 // rr: the row's n records (column order).  orec (optional) receives the
 // merged record; vals/idx (optional) the row's final k outputs; a bad row is
-// flagged as bad_row in ws when `flag`.
-template <int KC, int NT, bool CG>
+// flagged as bad_row in ws when `flag`.  Threads 0..NT-1 take part; `sync`
+// is their barrier (__syncthreads, or a named barrier when other warps of
+// the CTA have exited).
+template <int KC, int NT, bool CG, class Sync = CtaSync>
 __device__ __forceinline__ void combine_records_cta(const char* __restrict__ rr, int n, int k, int mode,
                                                     char* __restrict__ orec, float* __restrict__ vals,
                                                     long long* __restrict__ idx, void* ws, long long bad_row,
-                                                    bool flag, CombineSmem<KC, NT>& sm) {
+                                                    bool flag, CombineSmem<KC, NT>& sm, Sync sync = Sync()) {
   constexpr int NW = NT / 32;
   const int t = threadIdx.x, l = t & 31, w = t >> 5;
   const size_t rb = rec_bytes_(k);
@@ -627,9 +632,23 @@ __device__ __forceinline__ void combine_records_cta(const char* __restrict__ rr,
     for (int r = 0; r < KC; ++r)
       if (r < k) L.offer(cv[r], ci[r]);
   }
-  a = md_cta_reduce<NW>(a, sm.smf);
-  mn = cta_min<NW>(mn, sm.smf);
-  nan_seen = cta_sum<NW>(nan_seen, sm.smf);
+  // one round of CTA reductions: (m, d), min and the NaN count together
+  a = md_group_reduce<32>(a);
+  mn = group_min<32>(mn);
+  nan_seen = group_sum<32>(nan_seen);
+  if (l == 0) {
+    sm.sm_m[w] = a.m;
+    sm.sm_d[w] = a.d;
+    sm.sm_mn[w] = mn;
+    sm.sm_nan[w] = nan_seen;
+  }
+  sync();
+  a = l < NW ? MD{sm.sm_m[l], sm.sm_d[l]} : md_identity();
+  mn = l < NW ? sm.sm_mn[l] : -kNegInf;
+  nan_seen = l < NW ? sm.sm_nan[l] : 0.0f;
+  a = md_group_reduce<32>(a);
+  mn = group_min<32>(mn);
+  nan_seen = group_sum<32>(nan_seen);
   bool bad;
   if (mode == kModeFused)
     bad = !(a.d == a.d) || !isfinite(a.m) || mn == kNegInf || nan_seen > 0.0f;
@@ -644,7 +663,7 @@ __device__ __forceinline__ void combine_records_cta(const char* __restrict__ rr,
       sm.si[w * KC + r] = i;
     }
   });
-  __syncthreads();
+  sync();
   if (w == 0) {
     TopList<KC, long long> M;
     M.init(k);
@@ -670,6 +689,7 @@ __device__ __forceinline__ void combine_records_cta(const char* __restrict__ rr,
       if (flag && bad && ws) flag_bad_row(ws, bad_row);
     }
   }
+  sync();  // the scratch may be reused by the caller
 }
 
 template <int KC, int NT>
@@ -740,6 +760,14 @@ cudaError_t run_rows(const float* x, long long ldx, long long rows, long long V,
     const long long grid = std::min<long long>((rows + 3) / 4, 1LL << 30);
     if (pipe == 6)  // per-warp bulk-copy ring: 3 x 2 KB chunks in flight per warp
       k_topk_rows<32, 128, KC, MODE, 4, 7, -2><<<(unsigned)grid, 128, 0, st>>>(x, ldx, rows, V, k, vals, idx, ws, pf);
+    else if (pipe == 4 && osmx_host::tuning().topk_block != 128)
+      // one warp per CTA: the one wave of rows spreads over the SMs one warp
+      // at a time (27-28 per SM at 4000 rows) instead of in 4-warp CTAs
+      // (6 or 7 per SM: 24 vs 28 warps, the 24-warp SMs idle at the end).
+      // B200, 4000 rows (tools/runs/r2_i.sh): 16K -4.3%, 32K -1.2%, 64K
+      // -0.8%, 128K -0.4% time vs 4-warp CTAs.
+      k_topk_rows<32, 32, KC, MODE, 4, 28, -1><<<(unsigned)std::min<long long>(rows, 1LL << 30), 32, 0, st>>>(
+          x, ldx, rows, V, k, vals, idx, ws, pf);
     else if (pipe == 4)  // register double buffering, 2 x 4 float4s per lane
       k_topk_rows<32, 128, KC, MODE, 4, 7, -1><<<(unsigned)grid, 128, 0, st>>>(x, ldx, rows, V, k, vals, idx, ws, pf);
     else if (pipe == 5)  // register double buffering, 2 x 2 float4s per lane
@@ -851,6 +879,9 @@ cudaError_t run_split(const float* x, long long ldx, long long rows, long long V
       // whole problem, then one CTA-wide combine per row.
       const long long pc = topk_tma_piece_chunk(rows, V, k);
       const long long R = (V + pc - 1) / pc;
+      if (rows <= kWsMaxTickets && osmx_host::tuning().split_fuse == 1)  // combine fused (ticket)
+        return osmx_host::launch_topk_tma_records(MODE, x, ldx, rows * R, V, k, ws, st, (int)R, pc, col0, rec, vals,
+                                                  idx, out_rec);
       cudaError_t e = osmx_host::launch_topk_tma_records(MODE, x, ldx, rows * R, V, k, ws, st, (int)R, pc, col0, rec);
       if (e != cudaSuccess) return e;
       if (R >= 64)

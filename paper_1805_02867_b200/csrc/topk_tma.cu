@@ -93,7 +93,8 @@ template <int NCW, int STAGES, int KC, int MODE>
 __global__ void __launch_bounds__((NCW + 1) * 32, kTmaMinBlocks)
     k_topk_tma(const float* __restrict__ x, long long ldx, long long rows, long long V, int k,
                float* __restrict__ vals, long long* __restrict__ idx, void* ws, int R = 0, long long chunk = 0,
-               long long col0 = 0, char* __restrict__ rec = nullptr) {
+               long long col0 = 0, char* __restrict__ rec = nullptr, unsigned* __restrict__ tickets = nullptr,
+               char* __restrict__ out_rec = nullptr) {
   constexpr int NC = NCW * 32;
   constexpr int U = kChunk / 16 / NC;  // float4s per consumer thread per stage
   static_assert(U >= 1 && U * NC * 16 == kChunk, "chunk must split evenly");
@@ -104,7 +105,11 @@ __global__ void __launch_bounds__((NCW + 1) * 32, kTmaMinBlocks)
   float* smf = reinterpret_cast<float*>(empty + STAGES);  // 2*NCW
   float* sv = smf + 2 * NCW;                              // NCW*KC
   int* si = reinterpret_cast<int*>(sv + NCW * KC);        // NCW*KC
-  int* tsh = si + NCW * KC;                               // 2 (row parity)
+  int* tsh = si + NCW * KC;                               // 2 (row parity) + the last-piece flag
+  // Record mode with tickets: the consumer group of the CTA that finishes a
+  // row's last piece merges the row's R records (in piece order) and writes
+  // the row's outputs -- the split combine fused into this launch.
+  __shared__ CombineSmem<KC, NCW * 32> csm;
 
   // Record mode (rec != nullptr): "row" p is piece p % R of input row p / R,
   // columns [r * chunk, min(V, (r + 1) * chunk)), and writes a split record
@@ -245,6 +250,25 @@ __global__ void __launch_bounds__((NCW + 1) * 32, kTmaMinBlocks)
     });
     if (my) {
       if (t == 0) *reinterpret_cast<RecHdr*>(my) = hdr;  // non-finite pieces: flagged by the combine
+      if (tickets) {
+        const long long ir = row / R;
+        __threadfence();  // this thread's record stores, device-wide, before the ticket
+        named_sync(1, NC);
+        if (t == 0) {
+          const unsigned tk = atomicAdd(&tickets[ir], 1u);
+          tsh[2] = tk == (unsigned)(R - 1);
+          if (tk == (unsigned)(R - 1)) tickets[ir] = 0u;  // every other piece of the row has its ticket
+        }
+        named_sync(1, NC);
+        if (tsh[2]) {
+          __threadfence();
+          const size_t rb = rec_bytes_(k);
+          combine_records_cta<KC, NCW * 32, true>(rec + (size_t)ir * R * rb, R, k, MODE,
+                                                  out_rec ? out_rec + (size_t)ir * rb : nullptr,
+                                                  vals ? vals + ir * k : nullptr, vals ? idx + ir * k : nullptr, ws,
+                                                  ir, true, csm, [] { named_sync(1, NCW * 32); });
+        }
+      }
     } else if (bad && t == 0) {
       flag_bad_row(ws, row);
     }
@@ -257,7 +281,7 @@ constexpr int kStages = 4;  // 3 x 4 x 16 KB of ring per SM
 template <int KC, int MODE>
 size_t tma_smem() {
   return (size_t)kStages * kChunk + 2 * kStages * sizeof(uint64_t) + 2 * kNCW * sizeof(float) +
-         (size_t)kNCW * KC * (sizeof(float) + sizeof(int)) + 2 * sizeof(int);
+         (size_t)kNCW * KC * (sizeof(float) + sizeof(int)) + 3 * sizeof(int);
 }
 template <int KC, int MODE>
 int tma_per_sm() {
@@ -275,7 +299,7 @@ int tma_per_sm() {
 template <int KC, int MODE>
 cudaError_t run_tma(const float* x, long long ldx, long long rows, long long V, int k, float* vals,
                     long long* idx, void* ws, cudaStream_t st, int R = 0, long long chunk = 0, long long col0 = 0,
-                    char* rec = nullptr) {
+                    char* rec = nullptr, unsigned* tickets = nullptr, char* out_rec = nullptr) {
   auto kern = k_topk_tma<kNCW, kStages, KC, MODE>;
   const size_t smem = tma_smem<KC, MODE>();
   const int per_sm = tma_per_sm<KC, MODE>();
@@ -284,7 +308,8 @@ cudaError_t run_tma(const float* x, long long ldx, long long rows, long long V, 
     if (e != cudaSuccess) return e;
   }
   const long long grid = std::min<long long>(rows, (long long)per_sm * osmx_host::num_sms());
-  kern<<<(unsigned)grid, (kNCW + 1) * 32, smem, st>>>(x, ldx, rows, V, k, vals, idx, ws, R, chunk, col0, rec);
+  kern<<<(unsigned)grid, (kNCW + 1) * 32, smem, st>>>(x, ldx, rows, V, k, vals, idx, ws, R, chunk, col0, rec, tickets,
+                                                     out_rec);
   osmx_host::count_launch();
   return cudaGetLastError();
 }
@@ -292,8 +317,10 @@ cudaError_t run_tma(const float* x, long long ldx, long long rows, long long V, 
 template <int MODE>
 cudaError_t dispatch_tma(const float* x, long long ldx, long long rows, long long V, int k, float* vals,
                          long long* idx, void* ws, cudaStream_t st, int R = 0, long long chunk = 0,
-                         long long col0 = 0, char* rec = nullptr) {
-#define OSMX_TMA_CASE(KC) return run_tma<KC, MODE>(x, ldx, rows, V, k, vals, idx, ws, st, R, chunk, col0, rec)
+                         long long col0 = 0, char* rec = nullptr, unsigned* tickets = nullptr,
+                         char* out_rec = nullptr) {
+#define OSMX_TMA_CASE(KC) \
+  return run_tma<KC, MODE>(x, ldx, rows, V, k, vals, idx, ws, st, R, chunk, col0, rec, tickets, out_rec)
   if (k <= 1) OSMX_TMA_CASE(1);
   if (k <= 5) OSMX_TMA_CASE(5);
   if (k <= 8) OSMX_TMA_CASE(8);
@@ -318,9 +345,13 @@ long long topk_tma_slots(int k) {
   return (long long)per_sm * num_sms();
 }
 cudaError_t launch_topk_tma_records(int mode, const float* x, long long ldx, long long pieces, long long V, int k,
-                                    void* ws, cudaStream_t st, int R, long long chunk, long long col0, char* rec) {
+                                    void* ws, cudaStream_t st, int R, long long chunk, long long col0, char* rec,
+                                    float* vals, long long* idx, char* out_rec) {
+  // vals / out_rec given: the last piece of each row merges its records
+  // (ticket counters in the workspace header area), no combine launch
+  unsigned* tickets = (vals || out_rec) ? reinterpret_cast<unsigned*>(static_cast<char*>(ws) + kWsTicketsOff) : nullptr;
   if (mode == kModeFused)
-    return dispatch_tma<kModeFused>(x, ldx, pieces, V, k, nullptr, nullptr, ws, st, R, chunk, col0, rec);
-  return dispatch_tma<kModeTopkOf>(x, ldx, pieces, V, k, nullptr, nullptr, ws, st, R, chunk, col0, rec);
+    return dispatch_tma<kModeFused>(x, ldx, pieces, V, k, vals, idx, ws, st, R, chunk, col0, rec, tickets, out_rec);
+  return dispatch_tma<kModeTopkOf>(x, ldx, pieces, V, k, vals, idx, ws, st, R, chunk, col0, rec, tickets, out_rec);
 }
 }  // namespace osmx_host

@@ -109,9 +109,9 @@ __global__ void __launch_bounds__(kWideThreads, MINB)
   if (t == 0) *reinterpret_cast<RecHdr*>(my) = hdr;
 
   // ---- ticket: the last CTA of the row merges the row's records
-  __syncthreads();  // every record store of this CTA is issued
+  __threadfence();  // this thread's record stores, device-wide, before the ticket
+  __syncthreads();
   if (t == 0) {
-    __threadfence();  // ... and visible device-wide before the ticket
     const unsigned tk = atomicAdd(&tickets[row], 1u);
     s_last = tk == (unsigned)(cpr - 1);
     if (s_last) tickets[row] = 0u;  // every other CTA of the row has taken its ticket
