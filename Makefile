@@ -78,3 +78,14 @@ refsuite: $(REFSUITE)
 ifneq ($(wildcard $(REF)/tests/test_softmax.cpp),)
 all: refsuite
 endif
+
+# Diagnostic build (tools/c5_timeline.py): the library with per-CTA
+# %globaltimer stamps in the one-row dynamic-chunk top-K (OSMX_TIMELINE).
+TL_OBJS = $(patsubst $(SRC_DIR)/%.cu,build/tl/%.o,$(SRCS))
+build/tl/%.o: $(SRC_DIR)/%.cu $(HDRS)
+	@mkdir -p build/tl
+	$(NVCC) $(NVFLAGS) -DOSMX_TIMELINE -c $< -o $@ 2> build/tl/$*.ptxas.log || (cat build/tl/$*.ptxas.log; false)
+build/tl/libosmx_b200.so: $(TL_OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(TL_OBJS) -lcudart -ldl
+timeline: build/tl/libosmx_b200.so
+.PHONY: timeline

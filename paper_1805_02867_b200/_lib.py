@@ -10,6 +10,9 @@ import os
 from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "libosmx_b200.so"
+# Diagnostic builds only (tools/c5_timeline.py sets it to build/tl/...)
+if os.environ.get("OSMX_LIB_DIAG"):
+    LIB_PATH = Path(os.environ["OSMX_LIB_DIAG"]).resolve()
 
 # C-ABI status codes (include/osmx_b200.h)
 (OK, ERR_EMPTY, ERR_NON_FINITE, ERR_INVALID_K, ERR_INVALID_CHUNK, ERR_INVALID_ARG, ERR_CUDA, ERR_UNSUPPORTED,

@@ -399,7 +399,7 @@ osmx_status osmx_config_set(const char* key, int64_t value) {
     if (value != 0 && (value < 16 || value > 227)) return OSMX_ERR_INVALID_ARG;
     t.staged_kb = (int)value;
   } else if (!strcmp(key, "split_cta")) {
-    if (value < -1 || value > 3) return OSMX_ERR_INVALID_ARG;
+    if (value < -1 || value > 4) return OSMX_ERR_INVALID_ARG;
     t.split_cta = (int)value;
   } else if (!strcmp(key, "proj_bn")) {
     if (value != 0 && value != 128 && value != 224 && value != 256) return OSMX_ERR_INVALID_ARG;
@@ -416,6 +416,9 @@ osmx_status osmx_config_set(const char* key, int64_t value) {
   } else if (!strcmp(key, "tma")) {
     if (value < 0 || value > 2) return OSMX_ERR_INVALID_ARG;
     t.tma = (int)value;
+  } else if (!strcmp(key, "tma_cfg")) {
+    if (value < 0 || value > 2) return OSMX_ERR_INVALID_ARG;
+    t.tma_cfg = (int)value;
   } else if (!strcmp(key, "host_chunk_mb")) {
     if (value < 1) return OSMX_ERR_INVALID_ARG;
     g_host_chunk_mb = value;
@@ -436,6 +439,7 @@ int64_t osmx_config_get(const char* key) {
   if (!strcmp(key, "topk_block")) return t.topk_block;
   if (!strcmp(key, "split_fuse")) return t.split_fuse;
   if (!strcmp(key, "tma")) return t.tma;
+  if (!strcmp(key, "tma_cfg")) return t.tma_cfg;
   if (!strcmp(key, "l2_prefetch")) return t.l2_prefetch;
   if (!strcmp(key, "topk_u8")) return t.topk_u8;
   if (!strcmp(key, "topk_pipe")) return t.topk_pipe;

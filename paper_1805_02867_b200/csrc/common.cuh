@@ -223,7 +223,24 @@ struct L2Acc {
   bool huge = false;
 
   // Raise the reference for a batch whose max is bm (no-op if bm <= m).
+  // Ordinary logits take the branch-free path: n only grows, and the
+  // rescale 2^(n_old - n_new) is MUFU.EX2 of an integer <= 0 (exact; +0
+  // while n is still -inf).  Every batch of every lane used to take the
+  // divergent bm > m branch in some lane of the warp (ncu, configs[4]: 82%
+  // of the warp-batches); this is 7 instructions and no branch.
   __device__ __forceinline__ void raise(float bm) {
+    if (!huge && fabsf(bm) < kHugeX) {
+      const float nn = fmaxf(n, ceilf(bm * kLog2e));
+      d *= ex2(n - nn);
+      n = nn;
+      m = fmaxf(m, bm);
+    } else {
+      raise_slow(bm);
+    }
+  }
+  // Huge magnitudes (|bm| >= 2^20, +-inf), NaN, and threads already in
+  // natural units.
+  __device__ __forceinline__ void raise_slow(float bm) {
     if (bm > m) {
       if (fabsf(bm) < kHugeX) {
         const float nn = ceilf(bm * kLog2e);
@@ -252,16 +269,19 @@ struct L2Acc {
   __device__ __forceinline__ void add_batch(const float4 (&v)[U]) {
     float s = 0.0f;
     if (!huge) {
-      // paired FFMA2 / FADD2 (sm_100): the same roundings as the scalar
-      // fmaf(x, L, -n) terms and (a + b) + (c + e) sums, half the issue slots
+      // paired FFMA2 / FADD2 (sm_100): the terms round like scalar
+      // fmaf(x, L, -n); the batch sums in two float lanes, (a + c) + (b + e)
+      // per float4 -- 2 FFMA2 + 4 MUFU + 2 FADD2 per 4 elements
       const float2 L2 = make_float2(kLog2e, kLog2e), N2 = make_float2(-n, -n);
+      float2 s2 = make_float2(0.0f, 0.0f);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const float2 t0 = __ffma2_rn(make_float2(v[u].x, v[u].y), L2, N2);
         const float2 t1 = __ffma2_rn(make_float2(v[u].z, v[u].w), L2, N2);
-        const float2 p = __fadd2_rn(make_float2(ex2(t0.x), ex2(t1.x)), make_float2(ex2(t0.y), ex2(t1.y)));
-        s += p.x + p.y;  // (a + b) + (c + e)
+        const float2 p = __fadd2_rn(make_float2(ex2(t0.x), ex2(t0.y)), make_float2(ex2(t1.x), ex2(t1.y)));
+        s2 = __fadd2_rn(s2, p);
       }
+      s = s2.x + s2.y;
     } else {
 #pragma unroll
       for (int u = 0; u < U; ++u)
@@ -460,7 +480,8 @@ __device__ __forceinline__ double cta_sum_d(double v, double* scratch) {
 struct WsHeader {
   unsigned long long bad;  // 0 = all rows finite, else (INT64_MAX - first bad row)
   long long row_base;      // added to flagged row ids (host pipeline blocks)
-  unsigned long long pad[14];
+  unsigned long long chunk_ctr;  // dynamic chunk counter of the one-row TMA split (reset by its last CTA)
+  unsigned long long pad[13];
 };
 constexpr int kWsTicketsOff = 128;
 constexpr int kWsMaxTickets = 992;  // rows of one wide-row launch
@@ -589,33 +610,84 @@ struct TopList {
 // index asc, lane asc).  All lanes of the group receive winner r through
 // sink(r, value, index); the winning lane pops its head.  Lanes of one
 // group must hold indices in one coordinate system (same row / chunk base).
-// (An XOR-butterfly that swaps whole lists per level and re-sorts with a
-// compare-exchange network was measured slower on B200 -- more instructions
-// for a chain that is not the bottleneck: 4000 x 32K fused top-K 0.0920 vs
-// 0.0898 ms, configs[4] 0.067 vs 0.063 ms, tools/runs/r2_k.sh.)
+//
+// WIDTH == 32: each round is a handful of warp-wide REDUX reductions (max of
+// the ordered value key, then min of the index among the lanes holding it)
+// instead of a 5-level shuffle butterfly carrying (value, index, lane):
+// ~12 instructions and 3 dependent reductions per round instead of ~60.
+// The key maps -0.0 to +0.0 (the reference's float compare ties them); the
+// winner's own value is broadcast, so a -0.0 keeps its sign bit.
+__device__ __forceinline__ int ord_key(float v) {
+  const int i = __float_as_int(v + 0.0f);  // -0 -> +0 (round to nearest)
+  return i ^ ((i >> 31) & 0x7fffffff);
+}
 template <int WIDTH, int KC, class I, class Sink>
 __device__ __forceinline__ void group_merge(TopList<KC, I>& L, int k, Sink&& sink) {
   const int lane = (int)(threadIdx.x & 31u);
-  for (int r = 0; r < k; ++r) {
-    float bv = L.v[0];
-    I bi = L.i[0];
-    int bl = lane;
-#pragma unroll
-    for (int o = WIDTH / 2; o > 0; o >>= 1) {
-      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      const I oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
-      const bool take = ov > bv || (ov == bv && (idx_less(oi, bi) || (oi == bi && ol < bl)));
-      if (take) {
-        bv = ov;
-        bi = oi;
-        bl = ol;
+  if constexpr (WIDTH == 32) {
+    for (int r = 0; r < k; ++r) {
+      const int kv = ord_key(L.v[0]);
+      const int mx = __reduce_max_sync(0xffffffffu, kv);
+      const bool top = kv == mx;
+      I bi;
+      bool win;
+      if constexpr (sizeof(I) == 8) {
+        const unsigned long long u = top ? static_cast<unsigned long long>(L.i[0]) : ~0ull;
+        const unsigned h = __reduce_min_sync(0xffffffffu, static_cast<unsigned>(u >> 32));
+        const unsigned l = __reduce_min_sync(0xffffffffu, static_cast<unsigned>(u >> 32) == h
+                                                              ? static_cast<unsigned>(u) : 0xffffffffu);
+        const unsigned long long w = (static_cast<unsigned long long>(h) << 32) | l;
+        bi = static_cast<I>(w);
+        win = top && u == w;
+      } else {
+        const unsigned u = top ? static_cast<unsigned>(L.i[0]) : 0xffffffffu;
+        const unsigned m = __reduce_min_sync(0xffffffffu, u);
+        bi = static_cast<I>(m);
+        win = top && u == m;
       }
+      const int bl = __ffs(__ballot_sync(0xffffffffu, win)) - 1;  // lowest lane on a full tie
+      const float bv = __shfl_sync(0xffffffffu, L.v[0], bl);
+      if (lane == bl) L.pop();
+      sink(r, bv, bi);
     }
-    if (lane == bl) L.pop();
-    sink(r, bv, bi);
+  } else {
+    for (int r = 0; r < k; ++r) {
+      float bv = L.v[0];
+      I bi = L.i[0];
+      int bl = lane;
+#pragma unroll
+      for (int o = WIDTH / 2; o > 0; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const I oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
+        const bool take = ov > bv || (ov == bv && (idx_less(oi, bi) || (oi == bi && ol < bl)));
+        if (take) {
+          bv = ov;
+          bi = oi;
+          bl = ol;
+        }
+      }
+      if (lane == bl) L.pop();
+      sink(r, bv, bi);
+    }
   }
 }
+
+// Diagnostic builds only (make timeline, -DOSMX_TIMELINE): %globaltimer
+// stamps at fixed points of the one-row combine (tools/c5_timeline.py).
+#ifdef OSMX_TIMELINE
+__device__ unsigned long long g_tl2[16];
+#define OSMX_STAMP(i)                                                          \
+  do {                                                                         \
+    if ((threadIdx.x & 31) == 0) {                                             \
+      unsigned long long t_;                                                   \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                   \
+      atomicMax(&g_tl2[(i)], t_);                                              \
+    }                                                                          \
+  } while (0)
+#else
+#define OSMX_STAMP(i) do { } while (0)
+#endif
 
 // Programmatic dependent launch: a kernel launched with launch_pdl may be
 // scheduled while the previous kernel in the stream drains; it must call

@@ -47,7 +47,7 @@ struct Tuning {
   int staged_kb = 0;            // staged softmax: ring (shared memory) per CTA, KB (0 auto)
   int split_cta = -1;           // top-K split path: -1 auto, 0 warp-per-piece records, 1 CTA-per-chunk
                                 // (legacy), 2 TMA-ring CTA per piece, 3 one-launch grid-stride
-                                // (topk_wide.cu)
+                                // (topk_wide.cu), 4 one row: TMA ring over dynamic chunks
   int proj_bn = 0;              // fused projection vocabulary tile (0 auto; 128, 256)
   int topk_pipe = 0;            // warp-per-row top-K via a cp.async smem pipeline (0 off; 1..3 layouts)
   int topk_u8 = -1;             // warp-per-row top-K with 8 float4s in flight (-1 auto)
@@ -57,6 +57,7 @@ struct Tuning {
   int topk_block = 0;           // threads per CTA of the one-wave warp-per-row top-K (0 auto = 32, 32, 128)
   int tma = 0;                  // TMA-ring top-K: 0 off (default: the warp-per-row
                                 // LDG kernel measures faster), 1 auto, 2 force
+  int tma_cfg = 0;              // TMA-ring layout for fused k <= 5 (topk_tma.cu TmaCfg: 0, 1, 2)
 };
 // The knobs in force for the current call on this thread.  osmx_config_set
 // writes process-wide defaults; every C-ABI entry point opens a TuningScope,
@@ -151,6 +152,10 @@ size_t topk_large_ws(long long rows, long long V, int k);
 // TMA-ring top-K in record mode (split path): resident CTAs on the device
 // for this k, and the launch over rows * R pieces of `chunk` columns.
 long long topk_tma_slots(int k);
+// One row, dynamic stage-sized chunks claimed from a workspace counter, one
+// record per resident CTA, the last CTA merges (topk_tma.cu).
+cudaError_t launch_topk_tma_dyn(int mode, const float* x, long long V, int k, float* vals, long long* idx, void* ws,
+                                cudaStream_t st, long long col0, char* rec, char* out_rec);
 // topk_wide.cu: one-launch grid-stride split with a fused last-CTA combine
 // (few rows, V < 2^31, rows <= 992): resident CTAs for this k and the launch.
 long long topk_wide_slots(int k);

@@ -105,11 +105,13 @@ struct Pass {
     const unsigned mask = __activemask();
     best = fmaxf(best, bkey);
     bool want = bkey > L.thr() && bkey >= T;
-    if (Tsh && __any_sync(mask, want)) {
+    // common case: one vote, no lane can admit anything
+    if (!__any_sync(mask, want)) return;
+    if (Tsh) {
       T = fmaxf(T, o2f(*reinterpret_cast<volatile int*>(Tsh)));  // other warps' progress
       want = bkey > L.thr() && bkey >= T;
     }
-    if (__any_sync(mask, want)) {
+    if (!Tsh || __any_sync(mask, want)) {
       // Raise T before inserting: the k-th largest of the lanes' bests
       // (this batch included) is a valid lower bound of the row's k-th best
       // (k distinct elements >= it), so only elements >= it are offered --
@@ -576,8 +578,9 @@ __global__ void __launch_bounds__(32)
 // in increasing index order and the cheap strict-'>' insertion keeps the
 // reference's tie order; the warp / CTA merges use the full order.
 // The body of the CTA-wide combine, shared with the one-launch wide-row
-// kernel (topk_wide.cu), where the records come from other CTAs of the same
-// launch: CG = true loads them L2-coherent (ld.global.cg) after the ticket.
+// kernel (topk_wide.cu) and the TMA record kernels (topk_tma.cu), where the
+// records come from other CTAs of the same launch: CG = true loads them
+// L2-coherent (ld.global.cg) after the ticket.
 template <int KC, int NT>
 struct CombineSmem {
   float sm_m[NT / 32], sm_d[NT / 32], sm_mn[NT / 32], sm_nan[NT / 32];
@@ -592,86 +595,141 @@ __device__ __forceinline__ T rec_ld(const T* p) {
 struct CtaSync {
   __device__ __forceinline__ void operator()() const { __syncthreads(); }
 };
-// rr: the row's n records (column order).  orec (optional) receives the
-// merged record; vals/idx (optional) the row's final k outputs; a bad row is
-// flagged as bad_row in ws when `flag`.  Threads 0..NT-1 take part; `sync`
-// is their barrier (__syncthreads, or a named barrier when other warps of
-// the CTA have exited).
-template <int KC, int NT, bool CG, class Sync = CtaSync>
+// One record's candidates as a left-aligned list (a record is sorted under
+// (value desc, index asc); slots past k hold (-inf, -1)).
+template <bool CG, int KC>
+__device__ __forceinline__ void rec_list(const char* my, int k, TopList<KC, long long>& L) {
+  const float* rv = reinterpret_cast<const float*>(my + rec_vals_off());
+  const long long* ri = reinterpret_cast<const long long*>(my + rec_idx_off(k));
+#pragma unroll
+  for (int r = 0; r < KC; ++r) {
+    L.v[r] = r < k ? rec_ld<CG>(rv + r) : kNegInf;
+    L.i[r] = r < k ? rec_ld<CG>(ri + r) : -1LL;
+  }
+}
+// k rounds of a warp arg-max where every lane holds TWO sorted lists: the
+// lane's candidate is the better of the two heads, and the winning lane
+// pops the list it came from -- the 2-way merge of each lane's lists is
+// folded into the warp merge, so a lane never builds a merged list.
+template <int KC, class Sink>
+__device__ __forceinline__ void group_merge2(TopList<KC, long long>& A, TopList<KC, long long>& B, int k,
+                                             Sink&& sink) {
+  const int lane = (int)(threadIdx.x & 31u);
+  for (int r = 0; r < k; ++r) {
+    const bool useB = TopList<KC, long long>::before_(B.v[0], B.i[0], A.v[0], A.i[0]);
+    const float hv = useB ? B.v[0] : A.v[0];
+    const long long hi = useB ? B.i[0] : A.i[0];
+    const int kv = ord_key(hv);
+    const int mx = __reduce_max_sync(0xffffffffu, kv);
+    const bool top = kv == mx;
+    const unsigned long long u = top ? static_cast<unsigned long long>(hi) : ~0ull;
+    const unsigned h = __reduce_min_sync(0xffffffffu, static_cast<unsigned>(u >> 32));
+    const unsigned lo =
+        __reduce_min_sync(0xffffffffu, static_cast<unsigned>(u >> 32) == h ? static_cast<unsigned>(u) : 0xffffffffu);
+    const unsigned long long wv = (static_cast<unsigned long long>(h) << 32) | lo;
+    const int bl = __ffs(__ballot_sync(0xffffffffu, top && u == wv)) - 1;
+    const float bv = __shfl_sync(0xffffffffu, hv, bl);
+    if (lane == bl) {
+      if (useB) B.pop();
+      else A.pop();
+    }
+    sink(r, bv, static_cast<long long>(wv));
+  }
+}
+// rr: the row's n records.  orec (optional) receives the merged record;
+// vals/idx (optional) the row's final k outputs; a bad row is flagged as
+// bad_row in ws when `flag`.  Threads 0..NT-1 take part; `sync` is their
+// barrier (__syncthreads, or a named barrier when other warps of the CTA
+// have exited).
+//
+// Latency-bound (one CTA at the end of a launch), so the critical path is
+// kept short: thread t loads records t and t + NT together (one L2 round
+// trip) as two sorted lists, merges their (m, d) (Eq. 4), and the warp
+// merge takes the better head of the two per round (group_merge2); records
+// past 2 * NT (rare) are inserted into the second list under the full
+// order.  Warp winners go through shared memory to warp 0, whose lanes hold
+// one warp's sorted list each.  Every merge level uses (value desc, index
+// asc), so any record order gives the reference's selection (COLS: the
+// records happen to be in column order -- kept for the callers' clarity).
+template <int KC, int NT, bool CG, class Sync = CtaSync, bool COLS = true>
 __device__ __forceinline__ void combine_records_cta(const char* __restrict__ rr, int n, int k, int mode,
                                                     char* __restrict__ orec, float* __restrict__ vals,
                                                     long long* __restrict__ idx, void* ws, long long bad_row,
                                                     bool flag, CombineSmem<KC, NT>& sm, Sync sync = Sync()) {
   constexpr int NW = NT / 32;
+  static_assert(NW <= 32, "warp 0 merges one list per warp");
   const int t = threadIdx.x, l = t & 31, w = t >> 5;
   const size_t rb = rec_bytes_(k);
-  MD a = md_identity();
-  float mn = -kNegInf;
-  float nan_seen = 0.0f;
-  TopList<KC, long long> L;
-  L.init(k);
-  for (int c = t; c < n; c += NT) {
-    // every field of the record is loaded before any is used (independent
-    // loads in flight together; the offers below branch)
-    const char* my = rr + (size_t)c * rb;
-    const float4 hv = rec_ld<CG>(reinterpret_cast<const float4*>(my));
-    const float* rv = reinterpret_cast<const float*>(my + rec_vals_off());
-    const long long* ri = reinterpret_cast<const long long*>(my + rec_idx_off(k));
-    float cv[KC];
-    long long ci[KC];
-#pragma unroll
-    for (int r = 0; r < KC; ++r) {
-      cv[r] = r < k ? rec_ld<CG>(rv + r) : kNegInf;
-      ci[r] = r < k ? rec_ld<CG>(ri + r) : -1LL;
-    }
-    const float hm = hv.x, hd = hv.y, hmn = hv.z;
-    a = md_merge(a, MD{hm, hd});
-    if (hmn != hmn) nan_seen = 1.0f;
-    mn = fminf(mn, hmn);
+  TopList<KC, long long> A, B;
+  A.init_empty();
+  B.init_empty();
+  float4 h0 = make_float4(kNegInf, 0.0f, -kNegInf, 0.0f), h1 = h0;  // (m, d, min, -) identities
+  if (t < n) {
+    h0 = rec_ld<CG>(reinterpret_cast<const float4*>(rr + (size_t)t * rb));
+    rec_list<CG>(rr + (size_t)t * rb, k, A);
+  }
+  if (t + NT < n) {
+    h1 = rec_ld<CG>(reinterpret_cast<const float4*>(rr + (size_t)(t + NT) * rb));
+    rec_list<CG>(rr + (size_t)(t + NT) * rb, k, B);
+  }
+  OSMX_STAMP(0);
+  MD a = md_merge(MD{h0.x, h0.y}, MD{h1.x, h1.y});
+  float mn = fminf(h0.z, h1.z);
+  float nan_seen = (h0.z != h0.z || h1.z != h1.z) ? 1.0f : 0.0f;
+  for (int c = t + 2 * NT; c < n; c += NT) {
+    const float4 hv = rec_ld<CG>(reinterpret_cast<const float4*>(rr + (size_t)c * rb));
+    TopList<KC, long long> C;
+    rec_list<CG>(rr + (size_t)c * rb, k, C);
+    a = md_merge(a, MD{hv.x, hv.y});
+    if (hv.z != hv.z) nan_seen = 1.0f;
+    mn = fminf(mn, hv.z);
 #pragma unroll
     for (int r = 0; r < KC; ++r)
-      if (r < k) L.offer(cv[r], ci[r]);
+      if (r < k) B.offer_ordered(C.v[r], C.i[r]);
   }
   // one round of CTA reductions: (m, d), min and the NaN count together
   a = md_group_reduce<32>(a);
   mn = group_min<32>(mn);
   nan_seen = group_sum<32>(nan_seen);
+  OSMX_STAMP(1);
+  group_merge2(A, B, k, [&](int r, float v, long long i) {
+    if (l == 0) {
+      sm.sv[w * KC + r] = v;
+      sm.si[w * KC + r] = i;
+    }
+  });
   if (l == 0) {
     sm.sm_m[w] = a.m;
     sm.sm_d[w] = a.d;
     sm.sm_mn[w] = mn;
     sm.sm_nan[w] = nan_seen;
   }
+  OSMX_STAMP(2);
   sync();
-  a = l < NW ? MD{sm.sm_m[l], sm.sm_d[l]} : md_identity();
-  mn = l < NW ? sm.sm_mn[l] : -kNegInf;
-  nan_seen = l < NW ? sm.sm_nan[l] : 0.0f;
-  a = md_group_reduce<32>(a);
-  mn = group_min<32>(mn);
-  nan_seen = group_sum<32>(nan_seen);
-  bool bad;
-  if (mode == kModeFused)
-    bad = !(a.d == a.d) || !isfinite(a.m) || mn == kNegInf || nan_seen > 0.0f;
-  else
-    bad = nan_seen > 0.0f;
-  const double R = 1.0 / (double)a.d;
-  // per-warp k winners -> shared memory -> warp 0 merges NW * k candidates
-  L.normalize(k);
-  group_merge<32>(L, k, [&](int r, float v, long long i) {
-    if (l == 0) {
-      sm.sv[w * KC + r] = v;
-      sm.si[w * KC + r] = i;
-    }
-  });
-  sync();
+  OSMX_STAMP(3);
   if (w == 0) {
+    a = l < NW ? MD{sm.sm_m[l], sm.sm_d[l]} : md_identity();
+    mn = l < NW ? sm.sm_mn[l] : -kNegInf;
+    nan_seen = l < NW ? sm.sm_nan[l] : 0.0f;
+    a = md_group_reduce<32>(a);
+    mn = group_min<32>(mn);
+    nan_seen = group_sum<32>(nan_seen);
+    bool bad;
+    if (mode == kModeFused)
+      bad = !(a.d == a.d) || !isfinite(a.m) || mn == kNegInf || nan_seen > 0.0f;
+    else
+      bad = nan_seen > 0.0f;
+    const double R = 1.0 / (double)a.d;
     TopList<KC, long long> M;
-    M.init(k);
-    for (int q = l; q < NW * k; q += 32) {
-      const int ww = q / k, r = q % k;
-      M.offer_ordered(sm.sv[ww * KC + r], sm.si[ww * KC + r]);
+    M.init_empty();
+    if (l < NW) {
+#pragma unroll
+      for (int r = 0; r < KC; ++r)
+        if (r < k) {
+          M.v[r] = sm.sv[l * KC + r];
+          M.i[r] = sm.si[l * KC + r];
+        }
     }
-    M.normalize(k);
     group_merge<32>(M, k, [&](int r, float v, long long i) {
       if (l == (r & 31)) {
         if (orec) {
@@ -688,6 +746,7 @@ __device__ __forceinline__ void combine_records_cta(const char* __restrict__ rr,
       if (orec) *reinterpret_cast<RecHdr*>(orec) = RecHdr{a.m, a.d, nan_seen > 0.0f ? __int_as_float(0x7fffffff) : mn, k};
       if (flag && bad && ws) flag_bad_row(ws, bad_row);
     }
+    OSMX_STAMP(4);
   }
   sync();  // the scratch may be reused by the caller
 }
@@ -872,6 +931,8 @@ cudaError_t run_split(const float* x, long long ldx, long long rows, long long V
     // 64 x 1M 0.062 vs 0.068, 400 x 1M 0.270 vs 0.314; but 128 x 256K 0.045
     // vs 0.038.
     if (how < 0) how = (rows >= 64 && rows * V <= (1LL << 25)) ? 0 : 2;
+    if (how == 4 && rows == 1 && topk_wide_ok(rows, V))
+      return osmx_host::launch_topk_tma_dyn(MODE, x, V, k, vals, idx, ws, st, col0, rec, out_rec);
     if (how == 3 && topk_wide_ok(rows, V))
       return osmx_host::launch_topk_wide(MODE, x, ldx, rows, V, k, vals, idx, ws, st, col0, out_rec);
     if (how == 2) {
