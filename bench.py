@@ -793,13 +793,17 @@ def c1_parity(lib, _lib, dev) -> dict:
     return out
 
 
-def time_rotating(launch, n_sets: int, reps: int, graph: bool = True):
+def time_rotating(launch, n_sets: int, reps: int, graph: bool = True, graph_ms: float = 2.0):
     """Per-launch device time of `launch(i, stream_handle)` over n_sets
     distinct buffer sets launched back to back (set i's inputs were last
     touched n_sets-1 launches ago, so with n_sets * working set >= 4 x L2
-    every launch starts with its inputs out of L2).  The n_sets launches are
-    captured in one CUDA graph (no host launch gaps), timed with CUDA events
-    on the launching stream; returns (median ms per launch, min ms)."""
+    every launch starts with its inputs out of L2).  The launches are
+    captured in one CUDA graph (no host launch gaps): the rotation repeated
+    until the graph holds >= graph_ms of work (at most 64 launches), so the
+    graph's own launch latency (several us) is not charged to a short
+    kernel -- with 2 sets of a 4000 x 32K or a 2^26 row it used to add ~4 us
+    per launch.  Timed with CUDA events on the launching stream; returns
+    (median ms per launch, min ms)."""
     import torch
 
     s = torch.cuda.Stream()
@@ -807,14 +811,23 @@ def time_rotating(launch, n_sets: int, reps: int, graph: bool = True):
     with torch.cuda.stream(s):
         for i in range(n_sets):  # warm-up (and first-touch of every set)
             launch(i, s.cuda_stream)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for i in range(n_sets):  # a per-launch estimate to size the graph
+            launch(i, s.cuda_stream)
+        e1.record(s)
     torch.cuda.current_stream().wait_stream(s)
     torch.cuda.synchronize()
+    est = max(e0.elapsed_time(e1) / n_sets, 1e-4)
+    rounds = int(max(1, min(64 // n_sets, -(-graph_ms // (est * n_sets)))))
+    n_launch = rounds * n_sets
     g = None
     if graph:
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=s):
-            for i in range(n_sets):
-                launch(i, s.cuda_stream)
+            for j in range(n_launch):
+                launch(j % n_sets, s.cuda_stream)
         torch.cuda.synchronize()
     ts = []
     with torch.cuda.stream(s):
@@ -825,11 +838,11 @@ def time_rotating(launch, n_sets: int, reps: int, graph: bool = True):
             if g is not None:
                 g.replay()
             else:
-                for i in range(n_sets):
-                    launch(i, s.cuda_stream)
+                for j in range(n_launch):
+                    launch(j % n_sets, s.cuda_stream)
             b.record(s)
             b.synchronize()
-            ts.append(a.elapsed_time(b) / n_sets)
+            ts.append(a.elapsed_time(b) / n_launch)
     torch.cuda.synchronize()
     return statistics.median(ts), min(ts)
 

@@ -417,7 +417,7 @@ osmx_status osmx_config_set(const char* key, int64_t value) {
     if (value < 0 || value > 2) return OSMX_ERR_INVALID_ARG;
     t.tma = (int)value;
   } else if (!strcmp(key, "tma_cfg")) {
-    if (value < 0 || value > 2) return OSMX_ERR_INVALID_ARG;
+    if (value < -1 || value > 2) return OSMX_ERR_INVALID_ARG;
     t.tma_cfg = (int)value;
   } else if (!strcmp(key, "host_chunk_mb")) {
     if (value < 1) return OSMX_ERR_INVALID_ARG;

@@ -719,6 +719,7 @@ __device__ __forceinline__ void combine_records_cta(const char* __restrict__ rr,
       bad = !(a.d == a.d) || !isfinite(a.m) || mn == kNegInf || nan_seen > 0.0f;
     else
       bad = nan_seen > 0.0f;
+    OSMX_STAMP(7);
     const double R = 1.0 / (double)a.d;
     TopList<KC, long long> M;
     M.init_empty();
@@ -730,6 +731,7 @@ __device__ __forceinline__ void combine_records_cta(const char* __restrict__ rr,
           M.i[r] = sm.si[l * KC + r];
         }
     }
+    OSMX_STAMP(8);
     group_merge<32>(M, k, [&](int r, float v, long long i) {
       if (l == (r & 31)) {
         if (orec) {
@@ -930,9 +932,15 @@ cudaError_t run_split(const float* x, long long ldx, long long rows, long long V
     // vs warp pieces): 1 x 2^26 0.062 vs 0.067, 8 x 1M 0.026 vs 0.029,
     // 64 x 1M 0.062 vs 0.068, 400 x 1M 0.270 vs 0.314; but 128 x 256K 0.045
     // vs 0.038.
-    if (how < 0) how = (rows >= 64 && rows * V <= (1LL << 25)) ? 0 : 2;
-    if (how == 4 && rows == 1 && topk_wide_ok(rows, V))
-      return osmx_host::launch_topk_tma_dyn(MODE, x, V, k, vals, idx, ws, st, col0, rec, out_rec);
+    // One row (configs[4], the V-split slices): the TMA ring over dynamically
+    // claimed chunks, combine fused in the last CTA -- 1 x 2^26: 0.0521 ms
+    // vs 0.0558 for static pieces + a combine launch (tools/runs/r2_s.sh).
+    if (how < 0) how = rows == 1 ? 4 : (rows >= 64 && rows * V <= (1LL << 25)) ? 0 : 2;
+    if (how == 4) {
+      if (rows == 1 && topk_wide_ok(rows, V))
+        return osmx_host::launch_topk_tma_dyn(MODE, x, V, k, vals, idx, ws, st, col0, rec, out_rec);
+      how = 2;  // several rows, or 32-bit element indices overflow: static TMA pieces
+    }
     if (how == 3 && topk_wide_ok(rows, V))
       return osmx_host::launch_topk_wide(MODE, x, ldx, rows, V, k, vals, idx, ws, st, col0, out_rec);
     if (how == 2) {

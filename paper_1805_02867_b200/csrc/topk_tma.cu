@@ -435,36 +435,76 @@ __global__ void __launch_bounds__((NCW + 1) * 32, tma_min_blocks(STAGES * kChunk
     P.scalar(ld_f1(sg.p + j), j, k);
   }
 
-  // ---- this CTA's record
-  RecHdr hdr{kNegInf, 0.0f, 0.0f, k};
-  if constexpr (MODE == kModeFused) {
-    const MD tot = md_group_cta<NCW>(P.acc.finish(), smf);
-    const float mn = red_group_cta<NCW>(P.mn, -kNegInf, MinOp(), smf);
-    hdr = RecHdr{tot.m, tot.d, mn, k};
-  } else {
-    const float cc = red_group_cta<NCW>(P.chk, 0.0f, SumOp(), smf);
-    hdr.mn = (cc == cc) ? 0.0f : cc;
-  }
-  const size_t rb = rec_bytes_(k);
-  char* my = rec + (size_t)blockIdx.x * rb;
-  merge_group_cta<NCW>(P.L, k, sv, si, [&](int r, float v, int i) {
-    if ((int)(threadIdx.x & 31) == (r & 31)) {
-      reinterpret_cast<float*>(my + rec_vals_off())[r] = v;
-      reinterpret_cast<long long*>(my + rec_idx_off(k))[r] = i < 0 ? -1LL : (long long)i + col0;
+  // ---- this CTA's record, then the ticket: two barrier rounds.  Each warp
+  // reduces its (m, d, min) and merges its lanes' lists; warp 0 reduces the
+  // NCW warp results, writes the record, fences it and takes the ticket.
+  const int l = t & 31;
+  {
+    MD tot = md_identity();
+    float mn = -kNegInf;
+    if constexpr (MODE == kModeFused) {
+      tot = md_group_reduce<32>(P.acc.finish());
+      mn = group_min<32>(P.mn);
+    } else {
+      mn = group_sum<32>(P.chk);  // NaN iff some element was inf / NaN
     }
-  });
-  if (t == 0) *reinterpret_cast<RecHdr*>(my) = hdr;
-  __threadfence();  // this thread's record stores, device-wide, before the ticket
+    P.L.normalize(k);
+    group_merge<32>(P.L, k, [&](int r, float v, int i) {
+      if (l == 0) {
+        sv[w * KC + r] = v;
+        si[w * KC + r] = i;
+      }
+    });
+    if (l == 0) {
+      smf[w] = tot.m;
+      smf[NCW + w] = tot.d;
+      csm.sm_mn[w] = mn;
+    }
+  }
   named_sync(1, NC);
-  if (t == 0) {
-    const unsigned tk = atomicAdd(ticket, 1u);
-    s_last = tk == gridDim.x - 1;
+  if (w == 0) {
+    MD tot = l < NCW ? MD{smf[l], smf[NCW + l]} : md_identity();
+    float mn = l < NCW ? csm.sm_mn[l] : (MODE == kModeFused ? -kNegInf : 0.0f);
+    RecHdr hdr{kNegInf, 0.0f, 0.0f, k};
+    if constexpr (MODE == kModeFused) {
+      tot = md_group_reduce<32>(tot);
+      mn = group_min<32>(mn);
+      hdr = RecHdr{tot.m, tot.d, mn, k};
+    } else {
+      mn = group_sum<32>(mn);
+      hdr.mn = (mn == mn) ? 0.0f : mn;
+    }
+    const size_t rb = rec_bytes_(k);
+    char* my = rec + (size_t)blockIdx.x * rb;
+    TopList<KC> M;
+    M.init_empty();
+    if (l < NCW) {
+#pragma unroll
+      for (int r = 0; r < KC; ++r)
+        if (r < k) {
+          M.v[r] = sv[l * KC + r];
+          M.i[r] = si[l * KC + r];
+        }
+    }
+    group_merge<32>(M, k, [&](int r, float v, int i) {
+      if (l == (r & 31)) {
+        reinterpret_cast<float*>(my + rec_vals_off())[r] = v;
+        reinterpret_cast<long long*>(my + rec_idx_off(k))[r] = i < 0 ? -1LL : (long long)i + col0;
+      }
+    });
+    if (l == 0) *reinterpret_cast<RecHdr*>(my) = hdr;
+    __threadfence();  // the record, device-wide, before the ticket
+    __syncwarp();
+    if (l == 0) {
+      const unsigned tk = atomicAdd(ticket, 1u);
+      s_last = tk == gridDim.x - 1;
 #ifdef OSMX_TIMELINE
-    OSMX_TL(2, gtimer());
+      OSMX_TL(2, gtimer());
 #endif
-    if (s_last) {  // every CTA has claimed its last chunk and taken its ticket
-      ticket[0] = 0u;
-      hdr_ws->chunk_ctr = 0ull;
+      if (s_last) {  // every CTA has claimed its last chunk and taken its ticket
+        ticket[0] = 0u;
+        hdr_ws->chunk_ctr = 0ull;
+      }
     }
   }
   named_sync(1, NC);
@@ -553,8 +593,13 @@ cudaError_t run_tma_dyn(const float* x, long long V, int k, float* vals, long lo
 
 // The layout in force: the alternatives are built for the fused k <= 5 case
 // (configs[4] and the V-split slices) only.
-inline int tma_cfg_for(int k, int mode) {
-  const int c = osmx_host::tuning().tma_cfg;
+// Auto (-1): 8 x 3 x 32 KB for the one-row dynamic-chunk path (configs[4]:
+// 0.0521 vs 0.0528 ms for layout 0, 0.0558 for layout 2; tools/runs/r2_s.sh),
+// 8 x 4 x 16 KB for the static pieces (its one-wave piece count needs 3 CTAs
+// per SM).
+inline int tma_cfg_for(int k, int mode, bool dyn = false) {
+  int c = osmx_host::tuning().tma_cfg;
+  if (c < 0) c = dyn ? 1 : 0;
   return (mode == kModeFused && k > 1 && k <= 5) ? c : 0;
 }
 
@@ -620,7 +665,7 @@ long long topk_tma_slots(int k) {
 // One row, dynamic chunks, combine fused (records: one per resident CTA).
 cudaError_t launch_topk_tma_dyn(int mode, const float* x, long long V, int k, float* vals, long long* idx, void* ws,
                                 cudaStream_t st, long long col0, char* rec, char* out_rec) {
-  const int c = tma_cfg_for(k, mode);
+  const int c = tma_cfg_for(k, mode, true);
 #define OSMX_DYN(CFG, KC, MD) return run_tma_dyn<CFG, KC, MD>(x, V, k, vals, idx, ws, st, col0, rec, out_rec)
   if (mode == kModeFused) {
     if (k <= 1) OSMX_DYN(0, 1, kModeFused);

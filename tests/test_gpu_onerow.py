@@ -19,6 +19,9 @@ pytestmark = pytest.mark.gpu
 
 TOL = 1e-5
 PATHS = {
+    "auto": [],
+    "auto_split": [("shape", 3)],
+    "tma0": [("shape", 3), ("split_cta", 2), ("tma_cfg", 0)],
     "dyn0": [("shape", 3), ("split_cta", 4), ("tma_cfg", 0)],
     "dyn1": [("shape", 3), ("split_cta", 4), ("tma_cfg", 1)],
     "dyn2": [("shape", 3), ("split_cta", 4), ("tma_cfg", 2)],
@@ -33,7 +36,7 @@ def lib():
 
     _lib.load()
     yield _lib
-    for key, val in (("shape", 0), ("split_cta", -1), ("tma_cfg", 0), ("split_fuse", 0), ("split_chunk", 0)):
+    for key, val in (("shape", 0), ("split_cta", -1), ("tma_cfg", -1), ("split_fuse", 0), ("split_chunk", 0)):
         _lib.config_set(key, val)
 
 
@@ -71,7 +74,7 @@ def test_one_row_fused_and_topk_of(cuda, oracle_mod, lib, path, k):
             assert np.array_equal(tv.cpu().numpy().view(np.int32), qv.view(np.int32))
 
 
-@pytest.mark.parametrize("path", ["dyn0", "dyn1"])
+@pytest.mark.parametrize("path", ["auto", "dyn0", "dyn1"])
 def test_one_row_nonfinite(cuda, lib, path):
     """A NaN / +inf / -inf anywhere in the row (first, middle, last chunk,
     the scalar head or tail) raises NonFiniteError naming row 0."""

@@ -50,7 +50,7 @@ for cfg in (0, 1, 2):
         last = int(np.argmax(t[:, 2]))
         b2 = np.zeros(16, dtype=np.uint64)
         lib.osmx_diag_timeline2(b2.ctypes.data)
-        stamps = [(int(v) - int(t0)) / 1e3 if v else None for v in b2[:7]]
+        stamps = [(int(v) - int(t0)) / 1e3 if v else None for v in b2[:11]]
         spans.append(((t[:, 0] - t0) / 1e3, (t[:, 1] - t0) / 1e3, (t[:, 2] - t0) / 1e3, (t[last, 3] - t0) / 1e3,
                       t[:, 4]))
     s0, s1, s2, s3, ch = spans[-1]
@@ -61,5 +61,6 @@ for cfg in (0, 1, 2):
     print(f"   stream end min/med/max {s1.min():.2f} {np.median(s1):.2f} {s1.max():.2f} us")
     print(f"   ticket   min/med/max {s2.min():.2f} {np.median(s2):.2f} {s2.max():.2f} us; combine end {s3:.2f} us")
     print("   last CTA: fence in/out", stamps[5], stamps[6], "| loads done", stamps[0], "md/min reduced", stamps[1],
-          "warp merge", stamps[2], "sync", stamps[3], "final", stamps[4])
+          "warp merge", stamps[2], "sync", stamps[3], "w0 reduced", stamps[7],
+          "lists", stamps[8], "final", stamps[4])
     print(f"   chunks/CTA min/med/max {ch.min()} {int(np.median(ch))} {ch.max()}")

@@ -49,6 +49,7 @@ def main():
     for _ in range(a.rounds):
         for c in cfgs:
             kv = [p.split("=") for p in c.split(",") if p]
+            old = [(key, _lib.config_get(key)) for key, _ in kv]
             for key, val in kv:
                 _lib.config_set(key, int(val))
             nb = lib.osmx_workspace_bytes(alg, B, V, k if topk else 0)
@@ -65,8 +66,8 @@ def main():
 
             ms, _ = time_rotating(launch, n, a.reps)
             res[c].append(ms)
-            for key, _ in kv:
-                _lib.config_set(key, {"topk_u8": -1, "l2_prefetch": -1, "split_cta": -1}.get(key, 0))
+            for key, val in old:
+                _lib.config_set(key, val)
     for c in cfgs:
         ms = statistics.median(res[c])
         gbs = algo_bytes(a.alg, B, V, k) / (ms * 1e-3) / 1e9
