@@ -662,7 +662,11 @@ cudaError_t run_stream(const float* x, long long ldx, float* y, long long ldy, l
                        long long V, void* ws, cudaStream_t st) {
   int threads = osmx_host::tuning().stream_threads;
   const int pf = std::max(0, osmx_host::tuning().l2_prefetch);  // off unless forced (measured: mixed)
-  if (threads == 0) threads = V >= 65536 ? 512 : 256;
+  // 1024-thread CTAs for long rows (4000 rows, same box, tools/runs/r2_aa.sh):
+  // online 131K 0.840 vs 0.916 ms, 316K 2.247 vs 2.406, 562K 4.210 vs 4.490,
+  // 1M 7.109 vs 7.282; safe 316K 3.031 vs 3.147, 1M 9.428 vs 9.620.  The
+  // fp64-summing naive kernel prefers 512 (562K: 4.424 vs 4.640).
+  if (threads == 0) threads = V >= 65536 ? (ALG == osmx_host::kNaive ? 512 : 1024) : 256;
   const int keep = osmx_host::tuning().stream_ctas;  // > 0: persistent, CTAs per SM, evict-last pass 1
   if (keep > 0) {
     const long long grid = std::min<long long>(rows, (long long)keep * osmx_host::num_sms());
