@@ -985,11 +985,43 @@ def run_sweeps(lib, _lib, dev, sp, reps, peak) -> dict:
         out["topk"].append(row)
         del x
     out["c5"] = run_c5(lib, _lib, dev, reps, peak, l2, arena)
+    out["large_k"] = run_large_k(lib, _lib, dev, reps, peak, l2, arena)
     del arena
     torch.cuda.empty_cache()
     out["proj_fused"] = run_proj(dev, reps)
     torch.cuda.empty_cache()
     return out
+
+
+def run_large_k(lib, _lib, dev, reps, peak, l2, arena) -> dict:
+    """k above the register lists (radix select + ordered
+    compaction + sort, csrc/topk_large.cu) on the configs[2] row length,
+    4000 x 131072, fused online softmax + top-k for k = 5 (reference point),
+    33, 100 and 1000 -- algorithmic bytes 4V + 12k per row."""
+    import torch
+
+    B, V = 4000, 131072
+    n = n_rotating_sets(4 * B * V, l2)
+    x = arena.take(0, (n, B, V)).normal_()
+    res = {"rows": B, "V": V, "n_sets": n}
+    for k in (5, 33, 100, 1000):
+        vals = torch.empty((B, k), dtype=torch.float32, device=dev)
+        idx = torch.empty((B, k), dtype=torch.int64, device=dev)
+        alg = _lib.ONLINE_SOFTMAX_FUSED_TOPK
+        nb = lib.osmx_workspace_bytes(alg, B, V, k)
+        ws = torch.zeros(max(nb, 256), dtype=torch.uint8, device=dev)
+
+        def launch(i, st, ws=ws, k=k, vals=vals, idx=idx):
+            lib.osmx_softmax_topk(alg, x[i].data_ptr(), V, B, V, k, vals.data_ptr(), idx.data_ptr(), ws.data_ptr(),
+                                  ws.numel(), st)
+
+        ms, _ = time_rotating(launch, n, reps)
+        gbs = algo_bytes("online_fused", B, V, k) / (ms * 1e-3) / 1e9
+        res[f"k{k}"] = {"ms": round(ms, 5), "GBps": round(gbs, 1), "frac": round(gbs / peak, 3),
+                        "rows_per_s": round(B / (ms * 1e-3), 1)}
+        del ws, vals, idx
+    del x
+    return res
 
 
 def run_proj(dev, reps) -> dict:

@@ -9,9 +9,10 @@
 //
 //   warp 0        producer: lane 0 copies the CTA's slice of each row into a
 //                 D-slot shared-memory ring -- the 16-byte aligned body with
-//                 one 1-D bulk copy (cp.async.bulk, UBLKCP), the <= 3 + 3
-//                 edge elements with 4-byte cp.async -- completing on the
-//                 slot's "full" mbarrier; it runs up to D rows ahead.
+//                 one 1-D bulk copy (cp.async.bulk, UBLKCP) completing on the
+//                 slot's "full" mbarrier; it runs up to D rows ahead.  The
+//                 <= 3 + 3 edge elements are read from global memory by two
+//                 consumer threads.
 //   warps 1..     NG consumer groups of GW warps; group g takes the rows
 //                 g, g+NG, ... of its cluster.  Every pass of the algorithm
 //                 (online: (m, d) then scale; safe: max, sum, scale; naive:
@@ -45,14 +46,6 @@ namespace {
 
 using namespace osmx_dev;
 
-__device__ __forceinline__ void cp_async_4(float* dst, const float* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-// Arrive on `bar` once every cp.async this thread issued so far has landed
-// (noinc: the arrival is one of the barrier's expected arrivals).
-__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
 __device__ __forceinline__ void tma_load_1d_nohint(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
@@ -200,7 +193,7 @@ __global__ void __launch_bounds__(1024, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < D; ++s) {
-      mbar_init(&full[s], 2);    // expect_tx arrival + cp.async arrival
+      mbar_init(&full[s], 1);    // the producer's expect_tx arrival
       mbar_init(&empty[s], GW);  // one arrival per consumer warp of the group
     }
     for (int b = 0; b < 4 * NG; ++b) mbar_init(&recbar[b], 1);  // local expect_tx; C x 16 B of st.async
@@ -225,9 +218,7 @@ __global__ void __launch_bounds__(1024, 1)
         const int nvec = (n - head) >> 2;
         const int tail = n - head - 4 * nvec;
         float* sl = slots + (size_t)s * slotf + phase;  // sl[e] <- xs[e]
-        for (int e = 0; e < head; ++e) cp_async_4(sl + e, xs + e);
-        for (int e = n - tail; e < n; ++e) cp_async_4(sl + e, xs + e);
-        cp_async_mbar_arrive(&full[s]);
+        (void)tail;  // the <= 3 + 3 edge elements are read from global memory by the consumers
         mbar_arrive_expect_tx(&full[s], (uint32_t)nvec * 16u);
         if (nvec > 0) tma_load_1d_nohint(sl + head, xs + head, (uint32_t)nvec * 16u, &full[s]);
       }
@@ -259,13 +250,15 @@ __global__ void __launch_bounds__(1024, 1)
       const int qe0 = (phase && n > 0) ? 0 : -1;
       const int qe1 = (qb < nq && qb != qe0) ? qb : -1;
       const int my_edge = tg == 0 ? qe0 : (tg == 1 ? qe1 : -1);
+      // Edge float4s are not staged: their in-slice elements come from global
+      // memory (the slot's aligned body was the only bulk copy).
       auto masked = [&](int q, float fill) -> float4 {
-        float4 v = sl4[q];
         const int e0 = 4 * q - phase;
-        if (e0 + 0 < 0 || e0 + 0 >= n) v.x = fill;
-        if (e0 + 1 < 0 || e0 + 1 >= n) v.y = fill;
-        if (e0 + 2 < 0 || e0 + 2 >= n) v.z = fill;
-        if (e0 + 3 < 0 || e0 + 3 >= n) v.w = fill;
+        float4 v;
+        v.x = (e0 + 0 < 0 || e0 + 0 >= n) ? fill : ld_f1(xs + e0 + 0);
+        v.y = (e0 + 1 < 0 || e0 + 1 >= n) ? fill : ld_f1(xs + e0 + 1);
+        v.z = (e0 + 2 < 0 || e0 + 2 >= n) ? fill : ld_f1(xs + e0 + 2);
+        v.w = (e0 + 3 < 0 || e0 + 3 >= n) ? fill : ld_f1(xs + e0 + 3);
         return v;
       };
       auto min4 = [](float a, const float4& v) { return fminf(fminf(a, fminf(v.x, v.y)), fminf(v.z, v.w)); };
@@ -462,7 +455,7 @@ __global__ void __launch_bounds__(1024, 1)
         }
       }
       if (my_edge >= 0) {
-        const float4 v = sl4[my_edge];
+        const float4 v = masked(my_edge, 0.0f);
         const int e0 = 4 * my_edge - phase;
         if (e0 + 0 >= 0 && e0 + 0 < n) st_f1(ys + e0 + 0, f(v.x));
         if (e0 + 1 >= 0 && e0 + 1 < n) st_f1(ys + e0 + 1, f(v.y));
@@ -531,7 +524,7 @@ cudaError_t run_staged_cfg(const float* x, long long ldx, float* y, long long ld
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = C > 1 ? 1 : 0;  // a plain launch without a cluster
   long long ncl;
   if (C == 1) {
     // resident CTAs per SM from registers, threads and shared memory together

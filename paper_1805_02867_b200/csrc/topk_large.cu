@@ -252,6 +252,269 @@ __global__ void __launch_bounds__(kLT, 1)
   }
 }
 
+// ------------------------------------------------------------ fast path --
+// Fused online softmax + top-k and topk_of for 32 < k <= kFastK, two reads
+// of the row instead of five, no global sort:
+//   pass A  the row statistics (as above) and a 2048-bin histogram of the top
+//           11 bits of every key (shared-memory atomics);
+//   select  the bucket b* holding the k-th largest key (suffix scan);
+//   pass B  every element whose bucket is >= b* -- a superset of the top k,
+//           every tie at the k-th value included -- appended to shared
+//           memory (key, index); at most kFastCap of them;
+//   sort    a bitonic sort of the candidates under (key desc, index asc),
+//           the reference's order (topk.hpp:37-43), in shared memory; the
+//           first k are the answer, values re-read from x (so -0.0 keeps its
+//           sign in topk_of).
+// Rows whose boundary bucket is too full (heavy ties) take the radix path
+// (passes 2-3 and the ordered compaction above) into the workspace, then the
+// same shared-memory sort of their k candidates.
+constexpr int kFastK = 4096;
+constexpr int kFastCap = 8192;
+
+// (key desc, index asc): a precedes b
+__device__ __forceinline__ bool kbefore(unsigned ka, int ia, unsigned kb, int ib) {
+  return ka > kb || (ka == kb && ia < ib);
+}
+// Bitonic sort of P (a power of two <= kFastCap) entries, "before" first.
+__device__ __forceinline__ void smem_bitonic(unsigned* ck, int* ci, int P) {
+  for (int size = 2; size <= P; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < (P >> 1); i += kLT) {
+        const int lo = 2 * stride * (i / stride) + (i % stride), hi = lo + stride;
+        const bool up = (lo & size) == 0;  // this block ends "before"-first
+        const unsigned a = ck[lo], b = ck[hi];
+        const int ai = ci[lo], bi = ci[hi];
+        if (up ? kbefore(b, bi, a, ai) : kbefore(a, ai, b, bi)) {
+          ck[lo] = b;
+          ci[lo] = bi;
+          ck[hi] = a;
+          ci[hi] = ai;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// Suffix-scan bucket choice over nb buckets: sel[0] = the bucket holding
+// the krem-th largest, sel[1] = keys in higher buckets.
+__device__ __forceinline__ void pick_bucket(const unsigned* hist, int nb, int krem, unsigned* sel, int* smi) {
+  const int t = threadIdx.x;
+  const int r0 = 2 * t;  // reversed index: bucket nb-1-r
+  const unsigned c0 = r0 < nb ? hist[nb - 1 - r0] : 0u, c1 = r0 + 1 < nb ? hist[nb - 2 - r0] : 0u;
+  int pre, dummy, tot, dtot;
+  block_scan2((int)(c0 + c1), 0, pre, dummy, tot, dtot, smi);
+  if (r0 < nb) {
+    if (pre < krem && pre + (int)c0 >= krem) {
+      sel[0] = (unsigned)(nb - 1 - r0);
+      sel[1] = (unsigned)pre;
+    } else if (r0 + 1 < nb && pre + (int)c0 < krem && pre + (int)(c0 + c1) >= krem) {
+      sel[0] = (unsigned)(nb - 2 - r0);
+      sel[1] = (unsigned)(pre + c0);
+    }
+  }
+  __syncthreads();
+}
+
+// MODE: 0 fused online (key raw x, out e^(x-m)/d), 1 topk_of (raw).
+template <int MODE>
+__global__ void __launch_bounds__(kLT, 1)
+    k_topk_large_fast(const float* __restrict__ x, long long ldx, long long V, int k, float* __restrict__ vals,
+                      long long* __restrict__ idx, unsigned* __restrict__ ckey, int* __restrict__ cidx, void* ws) {
+  constexpr int U = 4;
+  extern __shared__ __align__(16) unsigned char fsm[];
+  unsigned* hist = reinterpret_cast<unsigned*>(fsm);        // 2048
+  unsigned* ck = hist + 2048;                                // kFastCap
+  int* ci = reinterpret_cast<int*>(ck + kFastCap);           // kFastCap
+  __shared__ float smf[2 * kLW];
+  __shared__ int smi[2 * kLW];
+  __shared__ unsigned sel[2];
+  __shared__ int ncand;
+  const long long row = blockIdx.x;
+  const int t = threadIdx.x;
+  const float* xr = x + row * ldx;
+  const Seg s = make_seg(xr, V);
+  for (int i = t; i < 2048; i += kLT) hist[i] = 0u;
+  if (t == 0) ncand = 0;
+  __syncthreads();
+
+  // pass A: statistics + top-11-bit histogram
+  auto h = [&](float v) { atomicAdd(&hist[fkey(v) >> 21], 1u); };
+  float M = 0.0f, R = 1.0f;
+  bool bad = false;
+  if constexpr (MODE == 0) {
+    L2Acc acc;
+    float mn = -kNegInf;
+    stream_seg<kLT, U, 2>(
+        s, t,
+        [&](float v, long long) {
+          mn = fminf(mn, v);
+          acc.add1(v);
+          h(v);
+        },
+        [&](float4 (&v)[U], long long, int cnt) {
+          float bm = kNegInf, bn = -kNegInf;
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            bm = fmaxf(bm, fmaxf(fmaxf(v[u].x, v[u].y), fmaxf(v[u].z, v[u].w)));
+            if (u < cnt) {
+              bn = fminf(bn, fminf(fminf(v[u].x, v[u].y), fminf(v[u].z, v[u].w)));
+              h(v[u].x), h(v[u].y), h(v[u].z), h(v[u].w);
+            }
+          }
+          mn = fminf(mn, bn);
+          acc.raise(bm);
+          acc.add_batch<U>(v);
+        });
+    const MD tot = md_cta_reduce<kLW>(acc.finish(), smf);
+    mn = cta_min<kLW>(mn, smf);
+    M = tot.m;
+    R = tot.d;
+    bad = !(tot.d == tot.d) || !isfinite(M) || mn == kNegInf;
+  } else {
+    float chk = 0.0f;
+    stream_seg<kLT, U, 2>(
+        s, t,
+        [&](float v, long long) {
+          chk = fmaf(v, 0.0f, chk);
+          h(v);
+        },
+        [&](float4 (&v)[U], long long, int cnt) {
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (u < cnt) {
+              chk = fmaf(v[u].x, 0.0f, fmaf(v[u].y, 0.0f, fmaf(v[u].z, 0.0f, fmaf(v[u].w, 0.0f, chk))));
+              h(v[u].x), h(v[u].y), h(v[u].z), h(v[u].w);
+            }
+        });
+    chk = cta_sum<kLW>(chk, smf);
+    bad = !(chk == chk);
+  }
+  if (t == 0 && bad) flag_bad_row(ws, row);
+  __syncthreads();  // histogram complete
+  pick_bucket(hist, 2048, k, sel, smi);
+  const unsigned bstar = sel[0];
+  const int total = (int)sel[1] + (int)hist[bstar];
+
+  int n;
+  if (total <= kFastCap) {
+    // pass B: the candidates (order of arrival is irrelevant: the sort uses
+    // the full (key, index) order)
+    auto take = [&](float v, long long j) {
+      const unsigned u = fkey(v);
+      if ((u >> 21) >= bstar) {
+        const int p = atomicAdd(&ncand, 1);
+        ck[p] = u;
+        ci[p] = (int)j;
+      }
+    };
+    stream_seg<kLT, U, 1>(
+        s, t, take,
+        [&](float4 (&v)[U], long long q0, int cnt) {
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            if (u >= cnt) break;
+            const long long j = body_index(s, q0 + (long long)u * kLT, 0);
+            if (((fkey(fmaxf(fmaxf(v[u].x, v[u].y), fmaxf(v[u].z, v[u].w))) >> 21) < bstar)) continue;
+            take(v[u].x, j), take(v[u].y, j + 1), take(v[u].z, j + 2), take(v[u].w, j + 3);
+          }
+        });
+    __syncthreads();
+    n = ncand;
+  } else {
+    // heavy ties at the boundary: exact radix select + ordered compaction of
+    // the k candidates (index order) into the workspace, then sort them here
+    unsigned* okey = ckey + row * (long long)k;
+    int* oidx = cidx + row * (long long)k;
+    unsigned prefix = 0, pmask = 0;
+    int krem = k;
+    const int shifts[3] = {21, 10, 0};
+    const int widths[3] = {11, 11, 10};
+#pragma unroll 1
+    for (int p = 0; p < 3; ++p) {
+      const int sh = shifts[p], nb = 1 << widths[p];
+      for (int i = t; i < nb; i += kLT) hist[i] = 0u;
+      __syncthreads();
+      auto add = [&](float v) {
+        const unsigned u = fkey(v);
+        if ((u & pmask) == prefix) atomicAdd(&hist[(u >> sh) & (nb - 1)], 1u);
+      };
+      stream_seg<kLT, U, 0>(
+          s, t, [&](float v, long long) { add(v); },
+          [&](float4 (&v)[U], long long, int cnt) {
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+              if (u < cnt) add(v[u].x), add(v[u].y), add(v[u].z), add(v[u].w);
+          });
+      __syncthreads();
+      pick_bucket(hist, nb, krem, sel, smi);
+      prefix |= sel[0] << sh;
+      pmask |= (unsigned)(nb - 1) << sh;
+      krem -= (int)sel[1];
+      __syncthreads();
+    }
+    const unsigned tau = prefix;
+    const int need_eq = krem;
+    int gt_base = 0, eq_base = 0;
+    for (long long base = 0; base < V; base += 4LL * kLT) {
+      unsigned kk[4];
+      int gt = 0, eq = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const long long e = base + 4LL * t + i;
+        kk[i] = e < V ? fkey(ld_f1(xr + e)) : 0u;
+        gt += (e < V && kk[i] > tau);
+        eq += (e < V && kk[i] == tau);
+      }
+      int gpre, epre, gtot, etot;
+      block_scan2(gt, eq, gpre, epre, gtot, etot, smi);
+      int gb = gt_base + gpre, ebf = eq_base + epre;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const long long e = base + 4LL * t + i;
+        if (e >= V) break;
+        if (kk[i] > tau) {
+          const int pos = gb + min(ebf, need_eq);
+          okey[pos] = kk[i];
+          oidx[pos] = (int)e;
+          ++gb;
+        } else if (kk[i] == tau) {
+          if (ebf < need_eq) {
+            const int pos = gb + ebf;
+            okey[pos] = kk[i];
+            oidx[pos] = (int)e;
+          }
+          ++ebf;
+        }
+      }
+      gt_base += gtot;
+      eq_base += etot;
+    }
+    __syncthreads();
+    for (int i = t; i < k; i += kLT) {
+      ck[i] = okey[i];
+      ci[i] = oidx[i];
+    }
+    n = k;
+  }
+  int P = 1;
+  while (P < n) P <<= 1;
+  for (int i = n + t; i < P; i += kLT) {  // pads sort last
+    ck[i] = 0u;
+    ci[i] = 0x7fffffff;
+  }
+  __syncthreads();
+  smem_bitonic(ck, ci, P);
+  const double rd = 1.0 / (double)R;
+  for (int r = t; r < k; r += kLT) {
+    const int j = ci[r];
+    float v = ld_f1(xr + j);  // the element itself (keeps -0.0)
+    if constexpr (MODE == 0) v = out_md(v, M, rd);  // kernels.hpp:122
+    vals[row * (long long)k + r] = v;
+    idx[row * (long long)k + r] = (long long)j;
+  }
+}
+
 __global__ void k_topk_large_offsets(int* off, long long rows, int k) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i <= rows; i += (long long)gridDim.x * blockDim.x)
     off[i] = (int)(i * k);
@@ -302,6 +565,20 @@ template <int MODE>
 cudaError_t run_large(const float* x, long long ldx, long long rows, long long V, int k, float* vals, long long* idx,
                       void* ws, char* region, cudaStream_t st) {
   const LargeLayout L = large_layout(rows, k);
+  if constexpr (MODE != 2) {
+    if (k <= kFastK) {
+      auto kern = k_topk_large_fast<MODE>;
+      const size_t smem = (2048 + 2 * (size_t)kFastCap) * 4;
+      if (osmx_host::first_use_on_device(reinterpret_cast<const void*>(kern))) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+      }
+      kern<<<(unsigned)rows, kLT, smem, st>>>(x, ldx, V, k, vals, idx, reinterpret_cast<unsigned*>(region + L.key_in),
+                                              reinterpret_cast<int*>(region + L.idx_in), ws);
+      osmx_host::count_launch();
+      return cudaGetLastError();
+    }
+  }
   unsigned* key_in = reinterpret_cast<unsigned*>(region + L.key_in);
   unsigned* key_out = reinterpret_cast<unsigned*>(region + L.key_out);
   int* idx_in = reinterpret_cast<int*>(region + L.idx_in);

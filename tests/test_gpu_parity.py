@@ -517,3 +517,29 @@ def test_safe_fused_topk_collisions_bit_exact(cuda, oracle_mod, lib, shape, V):
         # V = 100 the planted values' quotients land on distinct floats)
         if V >= 5003:
             assert (np.diff(rv, axis=1) == 0).any()
+
+
+@pytest.mark.parametrize("k", [33, 257, 4096])
+def test_large_k_fast_path_edges(cuda, oracle_mod, lib, k):
+    """The two-pass large-k path (csrc/topk_large.cu k_topk_large_fast):
+    a boundary bucket too full for shared memory (every key with the same
+    top 11 bits: the radix fallback), signed zeros kept in topk_of values,
+    candidates arriving in any order (bucket ties broken by index)."""
+    from paper_1805_02867_b200 import osmx
+
+    rng = np.random.default_rng(900 + k)
+    V = 20011
+    narrow = (1.0 + rng.random((3, V)) * 1e-3).astype(np.float32)  # one top-11-bit bucket
+    zeros = np.zeros((3, V), dtype=np.float32)
+    zeros[:, rng.choice(V, size=V // 2, replace=False)] = -0.0
+    spiky = rng.standard_normal((3, V)).astype(np.float32)
+    spiky[:, ::7] = 3.0  # many equal keys inside the boundary bucket
+    for x in (narrow, zeros, spiky):
+        vals, idx = osmx.softmax_topk(_dev(x), k, alg="online_fused")
+        fv, fz = _topk_ref(oracle_mod, "online_softmax_topk", x, k)
+        assert np.array_equal(idx.cpu().numpy(), fz)
+        assert max_rel(vals.cpu().numpy(), fv) <= TOL
+        tv, ti = osmx.topk(_dev(x), k)
+        rv, rz = _topk_ref(oracle_mod, "topk_of", x, k)
+        assert np.array_equal(ti.cpu().numpy(), rz)
+        assert np.array_equal(tv.cpu().numpy().view(np.int32), rv.view(np.int32))

@@ -23,6 +23,11 @@ IDS = {"naive": 0, "safe": 1, "online": 2, "safe_unfused": 3, "safe_fused": 4, "
 
 
 def main():
+    import faulthandler
+    import os
+
+    if os.environ.get("OSMX_WATCHDOG"):  # dump every thread's stack if a run hangs
+        faulthandler.dump_traceback_later(int(os.environ["OSMX_WATCHDOG"]), exit=True)
     ap = argparse.ArgumentParser()
     ap.add_argument("--alg", default="online_fused")
     ap.add_argument("--rows", type=int, default=4000)
