@@ -416,6 +416,9 @@ osmx_status osmx_config_set(const char* key, int64_t value) {
   } else if (!strcmp(key, "tma")) {
     if (value < 0 || value > 2) return OSMX_ERR_INVALID_ARG;
     t.tma = (int)value;
+  } else if (!strcmp(key, "large_fast")) {
+    if (value < 0 || value > 1) return OSMX_ERR_INVALID_ARG;
+    t.large_fast = (int)value;
   } else if (!strcmp(key, "tma_cfg")) {
     if (value < -1 || value > 2) return OSMX_ERR_INVALID_ARG;
     t.tma_cfg = (int)value;
@@ -440,6 +443,7 @@ int64_t osmx_config_get(const char* key) {
   if (!strcmp(key, "split_fuse")) return t.split_fuse;
   if (!strcmp(key, "tma")) return t.tma;
   if (!strcmp(key, "tma_cfg")) return t.tma_cfg;
+  if (!strcmp(key, "large_fast")) return t.large_fast;
   if (!strcmp(key, "l2_prefetch")) return t.l2_prefetch;
   if (!strcmp(key, "topk_u8")) return t.topk_u8;
   if (!strcmp(key, "topk_pipe")) return t.topk_pipe;

@@ -57,6 +57,7 @@ struct Tuning {
   int topk_block = 0;           // threads per CTA of the one-wave warp-per-row top-K (0 auto = 32, 32, 128)
   int tma = 0;                  // TMA-ring top-K: 0 off (default: the warp-per-row
                                 // LDG kernel measures faster), 1 auto, 2 force
+  int large_fast = 1;           // k > 32: two-pass shared-memory path (1) or the radix + CUB path (0)
   int tma_cfg = -1;             // TMA-ring layout for fused k <= 5 (topk_tma.cu TmaCfg: -1 auto, 0, 1, 2)
 };
 // The knobs in force for the current call on this thread.  osmx_config_set

@@ -236,7 +236,6 @@ __global__ void __launch_bounds__(1024, 1)
     for (long long row = cl + (long long)g * ncl; row < rows; row += (long long)NG * ncl, j += NG, ++k) {
       const int s = (int)(j % D);
       const int par = (int)(k & 1);
-      mbar_wait(&full[s], (uint32_t)((j / D) & 1));
       const float* xs = x + row * ldx + s0;
       float* ys = y + row * ldy + s0;
       const int phase = (int)((reinterpret_cast<uintptr_t>(xs) >> 2) & 3);
@@ -251,14 +250,23 @@ __global__ void __launch_bounds__(1024, 1)
       const int qe1 = (qb < nq && qb != qe0) ? qb : -1;
       const int my_edge = tg == 0 ? qe0 : (tg == 1 ? qe1 : -1);
       // Edge float4s are not staged: their in-slice elements come from global
-      // memory (the slot's aligned body was the only bulk copy).
+      // memory, loaded before the slot wait so the latency overlaps it.
+      float4 ev = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+      if (my_edge >= 0) {
+        const int e0 = 4 * my_edge - phase;
+        if (e0 + 0 >= 0 && e0 + 0 < n) ev.x = ld_f1(xs + e0 + 0);
+        if (e0 + 1 >= 0 && e0 + 1 < n) ev.y = ld_f1(xs + e0 + 1);
+        if (e0 + 2 >= 0 && e0 + 2 < n) ev.z = ld_f1(xs + e0 + 2);
+        if (e0 + 3 >= 0 && e0 + 3 < n) ev.w = ld_f1(xs + e0 + 3);
+      }
+      mbar_wait(&full[s], (uint32_t)((j / D) & 1));
       auto masked = [&](int q, float fill) -> float4 {
         const int e0 = 4 * q - phase;
         float4 v;
-        v.x = (e0 + 0 < 0 || e0 + 0 >= n) ? fill : ld_f1(xs + e0 + 0);
-        v.y = (e0 + 1 < 0 || e0 + 1 >= n) ? fill : ld_f1(xs + e0 + 1);
-        v.z = (e0 + 2 < 0 || e0 + 2 >= n) ? fill : ld_f1(xs + e0 + 2);
-        v.w = (e0 + 3 < 0 || e0 + 3 >= n) ? fill : ld_f1(xs + e0 + 3);
+        v.x = (e0 + 0 < 0 || e0 + 0 >= n) ? fill : ev.x;
+        v.y = (e0 + 1 < 0 || e0 + 1 >= n) ? fill : ev.y;
+        v.z = (e0 + 2 < 0 || e0 + 2 >= n) ? fill : ev.z;
+        v.w = (e0 + 3 < 0 || e0 + 3 >= n) ? fill : ev.w;
         return v;
       };
       auto min4 = [](float a, const float4& v) { return fminf(fminf(a, fminf(v.x, v.y)), fminf(v.z, v.w)); };
@@ -501,11 +509,26 @@ cudaError_t run_staged_cfg(const float* x, long long ldx, float* y, long long ld
   const size_t slot = (size_t)staged_slot_floats(Sv) * 4;
   ng = std::min(ng, 31 / GW);
   int D = 0;
+  // Ring depth vs groups of >= 4 warps: D >= NG + 2 once the ring has >= 5
+  // slots.  With 4-warp groups, (D, NG) = (5, 4), (6, 5), (7, 6), (8, 7) and
+  // once (7, 5) hung or faulted about once in 10^3-10^4 graph-replayed
+  // launches on B200 (tools/runs/r2_aq.sh, r2_ar.sh, r2_at.sh: 4000 rows at
+  // V = 7000-10000, including the previous defaults at 6500 < V <= 8192),
+  // while (4, 3), (5, 3) and every 1- and 2-warp-group layout (e.g. (7, 6)
+  // at V = 3162, thousands of sweep launches) ran clean.  The cause is not
+  // understood -- the slot protocol (one full / one empty mbarrier per slot,
+  // a group never more than one phase behind) checks out on paper -- so the
+  // defaults use 4-warp groups only with 3 groups (run_staged) and this
+  // guard covers the knobs.
   for (int it = 0; it < 3; ++it) {  // ng and the header size depend on each other (C > 1)
     const size_t avail = (size_t)std::min(ring_kb * 1024, kStagedSmemMax) - staged_slots_off(ng, C);
     D = (int)std::min<size_t>(avail / slot, kStagedMaxD);
-    if (D >= 2) ng = std::min(ng, D - 1);
+    if (D >= 5 && GW >= 4) ng = std::min(ng, D - 2);
+    else if (D >= 2) ng = std::min(ng, D - 1);
   }
+  // One-CTA rows above 8K elements: no deeper than NG + 1 = 4 slots (4000 x
+  // 10000: 0.0527 vs 0.0551 ms with 5 slots, tools/runs/r2_as.sh).
+  if (C == 1 && Sv > 8192 && tn.staged_kb == 0) D = std::min(D, ng + 1);
   if (D < 1 || ng < 1 || D < ng) return cudaErrorInvalidValue;
   const size_t smem = staged_slots_off(ng, C) + (size_t)D * slot;
   auto kern = k_softmax_staged<GW, ALG>;
@@ -575,7 +598,11 @@ cudaError_t run_staged(const float* x, long long ldx, float* y, long long ldy, l
   // two 100 KB CTAs per SM for short rows (4000 rows: 1778 -> 0.0156 vs 0.0205
   // ms, 3162 -> 0.0207 vs 0.0241), one 220 KB ring above
   const int kb = (C == 1 && Sv <= 4096) ? 100 : kClusterRingKB;
-  if (gw == 0) gw = Sv <= 1024 ? 1 : Sv <= 4096 ? 2 : (C > 1 && Sv > kClusterSlice) ? 8 : 4;
+  // 4-warp groups only with <= 3 groups: six 4-warp groups (slices of
+  // 4K-8K elements) hung or faulted now and then on B200 under long graph
+  // replays (see run_staged_cfg); six 2-warp groups, the layout of the
+  // shorter rows, run clean and as fast (4000 x 5623: 0.0316 vs 0.0312 ms).
+  if (gw == 0) gw = Sv <= 1024 ? 1 : Sv <= 8192 ? 2 : (C > 1 && Sv > kClusterSlice) ? 8 : 4;
   const int ng = gw == 1 ? 16 : Sv <= 8192 ? 6 : 3;
   switch (gw) {
     case 1: return run_staged_cfg<1, ALG>(x, ldx, y, ldy, rows, V, ws, st, ng, kb, C);

@@ -566,7 +566,7 @@ cudaError_t run_large(const float* x, long long ldx, long long rows, long long V
                       void* ws, char* region, cudaStream_t st) {
   const LargeLayout L = large_layout(rows, k);
   if constexpr (MODE != 2) {
-    if (k <= kFastK) {
+    if (k <= kFastK && osmx_host::tuning().large_fast) {
       auto kern = k_topk_large_fast<MODE>;
       const size_t smem = (2048 + 2 * (size_t)kFastCap) * 4;
       if (osmx_host::first_use_on_device(reinterpret_cast<const void*>(kern))) {
