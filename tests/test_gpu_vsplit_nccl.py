@@ -90,4 +90,6 @@ def test_vsplit_nonfinite_and_capture(cuda, comm):
             gv, gi = osmx.vsplit_softmax_topk_nccl(x, 0, 5, comm, check=False)
     g.replay()
     torch.cuda.synchronize()
-    assert torch.equal(gi, ref_i) and torch.equal(gv, ref_v)
+    # indices exact; values to fp32 rounding -- the one-row split assigns
+    # chunks to CTAs dynamically, so d's last bits follow the assignment
+    assert torch.equal(gi, ref_i) and torch.allclose(gv, ref_v, rtol=1e-6, atol=0)
