@@ -278,9 +278,10 @@ __device__ __forceinline__ bool kbefore(unsigned ka, int ia, unsigned kb, int ib
 // Bitonic sort of P (a power of two <= kFastCap) entries, "before" first.
 __device__ __forceinline__ void smem_bitonic(unsigned* ck, int* ci, int P) {
   for (int size = 2; size <= P; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+    for (int ls = __ffs(size) - 2; ls >= 0; --ls) {  // stride = 2^ls (shifts, no integer division)
+      const int stride = 1 << ls;
       for (int i = threadIdx.x; i < (P >> 1); i += kLT) {
-        const int lo = 2 * stride * (i / stride) + (i % stride), hi = lo + stride;
+        const int lo = ((i >> ls) << (ls + 1)) | (i & (stride - 1)), hi = lo + stride;
         const bool up = (lo & size) == 0;  // this block ends "before"-first
         const unsigned a = ck[lo], b = ck[hi];
         const int ai = ci[lo], bi = ci[hi];
