@@ -422,6 +422,54 @@ __global__ void __launch_bounds__(kLT, 1)
         });
     __syncthreads();
     n = ncand;
+    // Trim the candidates to (about) k before sorting: a radix select of the
+    // k-th largest key over the shared-memory candidates (3 digits), then keep
+    // every key > tau and every key == tau (ties, in any order; the sort
+    // puts the lowest indices first).  Sorting ~k instead of ~3k entries.
+    if (n > 2 * k) {
+      unsigned prefix = 0, pmask = 0;
+      int krem = k;
+      const int shifts[3] = {21, 10, 0};
+      const int widths[3] = {11, 11, 10};
+#pragma unroll 1
+      for (int p = 0; p < 3; ++p) {
+        const int sh = shifts[p], nb = 1 << widths[p];
+        for (int i = t; i < nb; i += kLT) hist[i] = 0u;
+        __syncthreads();
+        for (int i = t; i < n; i += kLT) {
+          const unsigned u = ck[i];
+          if ((u & pmask) == prefix) atomicAdd(&hist[(u >> sh) & (nb - 1)], 1u);
+        }
+        __syncthreads();
+        pick_bucket(hist, nb, krem, sel, smi);
+        prefix |= sel[0] << sh;
+        pmask |= (unsigned)(nb - 1) << sh;
+        krem -= (int)sel[1];
+        __syncthreads();
+      }
+      const unsigned tau = prefix;
+      constexpr int kPer = kFastCap / kLT;  // entries per thread (8)
+      unsigned kk[kPer];
+      int ii[kPer];
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) {
+        const int i = t + q * kLT;
+        kk[q] = i < n ? ck[i] : 0u;
+        ii[q] = i < n ? ci[i] : 0;
+      }
+      if (t == 0) ncand = 0;
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) {
+        if (t + q * kLT < n && kk[q] >= tau) {
+          const int pos = atomicAdd(&ncand, 1);
+          ck[pos] = kk[q];
+          ci[pos] = ii[q];
+        }
+      }
+      __syncthreads();
+      n = ncand;
+    }
   } else {
     // heavy ties at the boundary: exact radix select + ordered compaction of
     // the k candidates (index order) into the workspace, then sort them here
