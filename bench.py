@@ -793,7 +793,7 @@ def c1_parity(lib, _lib, dev) -> dict:
     return out
 
 
-def time_rotating(launch, n_sets: int, reps: int, graph: bool = True, graph_ms: float = 2.0):
+class RotTimer:
     """Per-launch device time of `launch(i, stream_handle)` over n_sets
     distinct buffer sets launched back to back (set i's inputs were last
     touched n_sets-1 launches ago, so with n_sets * working set >= 4 x L2
@@ -802,49 +802,76 @@ def time_rotating(launch, n_sets: int, reps: int, graph: bool = True, graph_ms: 
     until the graph holds >= graph_ms of work (at most 64 launches), so the
     graph's own launch latency (several us) is not charged to a short
     kernel -- with 2 sets of a 4000 x 32K or a 2^26 row it used to add ~4 us
-    per launch.  Timed with CUDA events on the launching stream; returns
-    (median ms per launch, min ms)."""
-    import torch
+    per launch.  times(reps) replays it, CUDA events on the launching
+    stream, and returns the per-launch ms of each replay; callers may
+    interleave several timers (rounds) so clock drift hits all alike."""
 
-    s = torch.cuda.Stream()
-    s.wait_stream(torch.cuda.current_stream())
-    with torch.cuda.stream(s):
-        for i in range(n_sets):  # warm-up (and first-touch of every set)
-            launch(i, s.cuda_stream)
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(s)
-        for i in range(n_sets):  # a per-launch estimate to size the graph
-            launch(i, s.cuda_stream)
-        e1.record(s)
-    torch.cuda.current_stream().wait_stream(s)
-    torch.cuda.synchronize()
-    est = max(e0.elapsed_time(e1) / n_sets, 1e-4)
-    rounds = int(max(1, min(64 // n_sets, -(-graph_ms // (est * n_sets)))))
-    n_launch = rounds * n_sets
-    g = None
-    if graph:
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=s):
-            for j in range(n_launch):
-                launch(j % n_sets, s.cuda_stream)
+    def __init__(self, launch, n_sets: int, graph: bool = True, graph_ms: float = 2.0):
+        import torch
+
+        self.launch, self.n_sets = launch, n_sets
+        s = self.s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for i in range(n_sets):  # warm-up (and first-touch of every set)
+                launch(i, s.cuda_stream)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            for i in range(n_sets):  # a per-launch estimate to size the graph
+                launch(i, s.cuda_stream)
+            e1.record(s)
+        torch.cuda.current_stream().wait_stream(s)
         torch.cuda.synchronize()
-    ts = []
-    with torch.cuda.stream(s):
-        for _ in range(reps):
-            a = torch.cuda.Event(enable_timing=True)
-            b = torch.cuda.Event(enable_timing=True)
-            a.record(s)
-            if g is not None:
-                g.replay()
-            else:
-                for j in range(n_launch):
+        est = max(e0.elapsed_time(e1) / n_sets, 1e-4)
+        rounds = int(max(1, min(64 // n_sets, -(-graph_ms // (est * n_sets)))))
+        self.n_launch = rounds * n_sets
+        self.g = None
+        if graph:
+            self.g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.g, stream=s):
+                for j in range(self.n_launch):
                     launch(j % n_sets, s.cuda_stream)
-            b.record(s)
-            b.synchronize()
-            ts.append(a.elapsed_time(b) / n_launch)
-    torch.cuda.synchronize()
+            torch.cuda.synchronize()
+
+    def times(self, reps: int) -> list:
+        import torch
+
+        ts = []
+        s = self.s
+        with torch.cuda.stream(s):
+            for _ in range(reps):
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record(s)
+                if self.g is not None:
+                    self.g.replay()
+                else:
+                    for j in range(self.n_launch):
+                        self.launch(j % self.n_sets, s.cuda_stream)
+                b.record(s)
+                b.synchronize()
+                ts.append(a.elapsed_time(b) / self.n_launch)
+        torch.cuda.synchronize()
+        return ts
+
+
+def time_rotating(launch, n_sets: int, reps: int, graph: bool = True, graph_ms: float = 2.0):
+    """RotTimer for one setting: (median ms per launch, min ms)."""
+    ts = RotTimer(launch, n_sets, graph, graph_ms).times(reps)
     return statistics.median(ts), min(ts)
+
+
+def time_interleaved(timers: dict, reps: int, rounds: int = 3) -> dict:
+    """Median per-launch ms of several RotTimers measured in `rounds`
+    interleaved rounds (each round replays every timer reps/rounds times),
+    so a slow stretch of the box hits every setting, not one."""
+    per = max(2, -(-reps // rounds))
+    ts = {k: [] for k in timers}
+    for _ in range(rounds):
+        for k, t in timers.items():
+            ts[k] += t.times(per)
+    return {k: (statistics.median(v), min(v)) for k, v in ts.items()}
 
 
 def n_rotating_sets(set_bytes: int, l2: int, cap_bytes: int = 48 << 30) -> int:
@@ -915,9 +942,10 @@ def run_sweeps(lib, _lib, dev, sp, reps, peak) -> dict:
                max(n_rotating_sets(4 * B * V, l2) * B * V for V in Vt_all), 2 * n_rotating_sets(8 << 26, l2) << 26)
     arena = Arena(need, dev)
     dram = dram_cells()
-    out = {"batch": B, "k": k, "timing": "CUDA graph of n_sets launches over rotating buffer sets "
-                                          "(>= 4 x L2, inputs cold in L2), CUDA events, median; one "
-                                          "preallocated arena for all buffers",
+    out = {"batch": B, "k": k, "timing": "CUDA graph of >= 2 ms of launches over rotating buffer sets "
+                                          "(>= 4 x L2, inputs cold in L2), CUDA events, median over 3 "
+                                          "rounds interleaving the algorithms of a V; one preallocated "
+                                          "arena for all buffers",
            "dram_bytes_source": dram.get("_source"), "softmax": [], "topk": []}
     Vs = Vs_all
     for V in Vs:
@@ -928,18 +956,23 @@ def run_sweeps(lib, _lib, dev, sp, reps, peak) -> dict:
         # best kernel family per V (auto), and the paper's one-CTA-per-row
         # streaming kernels (shape 2: every pass reads global memory; the
         # safe baseline of the north star, 3 passes / 4 accesses)
-        for name, alg, shape in (("naive", _lib.NAIVE_SOFTMAX, 0), ("safe", _lib.SAFE_SOFTMAX, 0),
-                                 ("online", _lib.ONLINE_SOFTMAX, 0), ("safe_stream", _lib.SAFE_SOFTMAX, 2),
-                                 ("online_stream", _lib.ONLINE_SOFTMAX, 2)):
-            _lib.config_set("shape", shape)
+        algs = (("naive", _lib.NAIVE_SOFTMAX, 0), ("safe", _lib.SAFE_SOFTMAX, 0), ("online", _lib.ONLINE_SOFTMAX, 0),
+                ("safe_stream", _lib.SAFE_SOFTMAX, 2), ("online_stream", _lib.ONLINE_SOFTMAX, 2))
+        timers, keep = {}, []
+        for name, alg, shape in algs:
+            _lib.config_set("shape", shape)  # in force while the graph is captured
             nb = lib.osmx_workspace_bytes(alg, B, V, 0)
             ws = torch.zeros(max(nb, 256), dtype=torch.uint8, device=dev)
+            keep.append(ws)
 
             def launch(i, st, alg=alg, ws=ws):
                 lib.osmx_softmax(alg, x[i].data_ptr(), V, y[i].data_ptr(), V, B, V, ws.data_ptr(), ws.numel(), st)
 
-            ms, ms_min = time_rotating(launch, n, reps)
+            timers[name] = RotTimer(launch, n)
             _lib.config_set("shape", 0)
+        meas = time_interleaved(timers, reps)
+        for name, alg, shape in algs:
+            ms, ms_min = meas[name]
             gbs = algo_bytes(name.replace("_stream", ""), B, V) / (ms * 1e-3) / 1e9
             row[name] = {"ms": round(ms, 5), "GBps": round(gbs, 1), "frac": round(gbs / peak, 3),
                          "dram_floor_GBps": round(8 * B * V / (ms * 1e-3) / 1e9, 1),
@@ -950,33 +983,39 @@ def run_sweeps(lib, _lib, dev, sp, reps, peak) -> dict:
         row["online_stream_over_safe_stream"] = round(row["safe_stream"]["ms"] / row["online_stream"]["ms"], 3)
         row["online_over_safe_stream"] = round(row["safe_stream"]["ms"] / row["online"]["ms"], 3)
         out["softmax"].append(row)
-        del x, y
+        del timers, keep, x, y
     for V in Vt_all:
         n = n_rotating_sets(4 * B * V, l2)
         x = arena.take(0, (n, B, V)).normal_()
         vals = torch.empty((B, k), dtype=torch.float32, device=dev)
         idx = torch.empty((B, k), dtype=torch.int64, device=dev)
         row = {"V": V, "n_sets": n}
-        for name, alg, shape in (("online_fused", _lib.ONLINE_SOFTMAX_FUSED_TOPK, 0),
-                                 ("online_unfused", _lib.ONLINE_SOFTMAX_UNFUSED_TOPK, 0),
-                                 ("safe_unfused", _lib.SAFE_SOFTMAX_UNFUSED_TOPK, 0),
-                                 ("safe_fused", _lib.SAFE_SOFTMAX_FUSED_TOPK, 0),
-                                 ("online_unfused_stream", _lib.ONLINE_SOFTMAX_UNFUSED_TOPK, 2)):
-            _lib.config_set("shape", shape)
+        algs = (("online_fused", _lib.ONLINE_SOFTMAX_FUSED_TOPK, 0),
+                ("online_unfused", _lib.ONLINE_SOFTMAX_UNFUSED_TOPK, 0),
+                ("safe_unfused", _lib.SAFE_SOFTMAX_UNFUSED_TOPK, 0),
+                ("safe_fused", _lib.SAFE_SOFTMAX_FUSED_TOPK, 0),
+                ("online_unfused_stream", _lib.ONLINE_SOFTMAX_UNFUSED_TOPK, 2))
+        timers, keep = {}, []
+        for name, alg, shape in algs:
+            _lib.config_set("shape", shape)  # in force while the graph is captured
             nb = lib.osmx_workspace_bytes(alg, B, V, k)
             ws = torch.zeros(max(nb, 256), dtype=torch.uint8, device=dev)
+            keep.append(ws)
 
             def launch(i, st, alg=alg, ws=ws):
                 lib.osmx_softmax_topk(alg, x[i].data_ptr(), V, B, V, k, vals.data_ptr(), idx.data_ptr(),
                                       ws.data_ptr(), ws.numel(), st)
 
-            ms, ms_min = time_rotating(launch, n, reps)
+            timers[name] = RotTimer(launch, n)
             _lib.config_set("shape", 0)
+        meas = time_interleaved(timers, reps)
+        for name, alg, shape in algs:
+            ms, ms_min = meas[name]
             gbs = algo_bytes(name.replace("_stream", ""), B, V) / (ms * 1e-3) / 1e9
             row[name] = {"ms": round(ms, 5), "GBps": round(gbs, 1), "frac": round(gbs / peak, 3),
                          "rows_per_s": round(B / (ms * 1e-3), 1)}
             add_dram(row[name], dram, name, V, ms, peak)
-            del ws
+        del timers, keep
         row["fused_over_online_unfused"] = round(row["online_unfused"]["ms"] / row["online_fused"]["ms"], 3)
         row["fused_over_safe_unfused"] = round(row["safe_unfused"]["ms"] / row["online_fused"]["ms"], 3)
         # unfused pipeline whose softmax stage is the paper's 3-access streaming kernel

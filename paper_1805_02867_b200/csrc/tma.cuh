@@ -63,8 +63,12 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
 }
 
 // Named barrier over the consumer warps only (the producer warp never joins).
+// The non-.aligned barrier.sync: arrival is per thread, so a warp that is
+// still diverged from a lane-0-only store or an mbarrier wait loop is
+// counted correctly (bar.sync = barrier.sync.aligned requires a converged
+// warp; the compiler need not reconverge before it).
 __device__ __forceinline__ void named_sync(int id, int nthreads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+  asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
 }  // namespace osmx_dev

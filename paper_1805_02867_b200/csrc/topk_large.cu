@@ -29,6 +29,16 @@ using namespace osmx_dev;
 
 namespace {
 
+// Block barrier after divergent code (per-lane atomics, predicated
+// candidate appends): the non-.aligned barrier.sync, whose arrival is per
+// thread -- the .aligned bar.sync that __syncthreads() emits requires a
+// converged warp, and compute-sanitizer synccheck flagged this kernel's
+// barriers after the candidate appends.
+__device__ __forceinline__ void cta_sync() {
+  __syncwarp();
+  asm volatile("barrier.sync 0;" ::: "memory");
+}
+
 constexpr int kLT = 1024;  // threads per row
 constexpr int kLW = kLT / 32;
 
@@ -52,7 +62,7 @@ __device__ __forceinline__ void block_scan2(int a, int b, int& a_pre, int& b_pre
     if (l >= o) ia += ta, ib += tb;
   }
   if (l == 31) sm[w] = ia, sm[kLW + w] = ib;
-  __syncthreads();
+  cta_sync();
   if (w == 0) {
     int va = l < kLW ? sm[l] : 0, vb = l < kLW ? sm[kLW + l] : 0;
 #pragma unroll
@@ -62,12 +72,12 @@ __device__ __forceinline__ void block_scan2(int a, int b, int& a_pre, int& b_pre
     }
     if (l < kLW) sm[l] = va, sm[kLW + l] = vb;  // inclusive over warps
   }
-  __syncthreads();
+  cta_sync();
   a_tot = sm[kLW - 1];
   b_tot = sm[2 * kLW - 1];
   a_pre = (w ? sm[w - 1] : 0) + ia - a;
   b_pre = (w ? sm[kLW + w - 1] : 0) + ib - b;
-  __syncthreads();
+  cta_sync();
 }
 
 // MODE: 0 fused online (key raw x, out e^(x-m)/d), 1 topk_of (raw), 2 safe (key p).
@@ -137,7 +147,7 @@ __global__ void __launch_bounds__(kLT, 1)
       M = cta_max<kLW>(m, smf);
       __shared__ double tab[32];
       exp2_tab_init(tab);
-      __syncthreads();
+      cta_sync();
       const double Md = (double)M;
       double d = 0.0;
       stream_seg<kLT, U, 0>(
@@ -174,7 +184,7 @@ __global__ void __launch_bounds__(kLT, 1)
   for (int p = 0; p < 3; ++p) {
     const int sh = shifts[p], nb = 1 << widths[p];
     for (int i = t; i < nb; i += kLT) hist[i] = 0u;
-    __syncthreads();
+    cta_sync();
     auto add = [&](float v) {
       const unsigned u = key(v);
       if ((u & pmask) == prefix) atomicAdd(&hist[(u >> sh) & (nb - 1)], 1u);
@@ -186,7 +196,7 @@ __global__ void __launch_bounds__(kLT, 1)
           for (int u = 0; u < U; ++u)
             if (u < cnt) add(v[u].x), add(v[u].y), add(v[u].z), add(v[u].w);
         });
-    __syncthreads();
+    cta_sync();
     // suffix counts: thread t owns buckets [2t, 2t+1] of the reversed order
     const int r0 = 2 * t;  // reversed index: bucket nb-1-r
     unsigned c0 = r0 < nb ? hist[nb - 1 - r0] : 0u, c1 = r0 + 1 < nb ? hist[nb - 2 - r0] : 0u;
@@ -202,11 +212,11 @@ __global__ void __launch_bounds__(kLT, 1)
         sel[1] = (unsigned)(pre + c0);
       }
     }
-    __syncthreads();
+    cta_sync();
     prefix |= sel[0] << sh;
     pmask |= (unsigned)(nb - 1) << sh;
     krem -= (int)sel[1];
-    __syncthreads();
+    cta_sync();
   }
   const unsigned tau = prefix;
   const int need_eq = krem;  // elements equal to tau to take (lowest indices)
@@ -292,7 +302,7 @@ __device__ __forceinline__ void smem_bitonic(unsigned* ck, int* ci, int P) {
           ci[hi] = ai;
         }
       }
-      __syncthreads();
+      cta_sync();
     }
   }
 }
@@ -314,7 +324,7 @@ __device__ __forceinline__ void pick_bucket(const unsigned* hist, int nb, int kr
       sel[1] = (unsigned)(pre + c0);
     }
   }
-  __syncthreads();
+  cta_sync();
 }
 
 // MODE: 0 fused online (key raw x, out e^(x-m)/d), 1 topk_of (raw).
@@ -337,7 +347,7 @@ __global__ void __launch_bounds__(kLT, 1)
   const Seg s = make_seg(xr, V);
   for (int i = t; i < 2048; i += kLT) hist[i] = 0u;
   if (t == 0) ncand = 0;
-  __syncthreads();
+  cta_sync();
 
   // pass A: statistics + top-11-bit histogram
   auto h = [&](float v) { atomicAdd(&hist[fkey(v) >> 21], 1u); };
@@ -392,7 +402,7 @@ __global__ void __launch_bounds__(kLT, 1)
     bad = !(chk == chk);
   }
   if (t == 0 && bad) flag_bad_row(ws, row);
-  __syncthreads();  // histogram complete
+  cta_sync();  // histogram complete
   pick_bucket(hist, 2048, k, sel, smi);
   const unsigned bstar = sel[0];
   const int total = (int)sel[1] + (int)hist[bstar];
@@ -420,7 +430,7 @@ __global__ void __launch_bounds__(kLT, 1)
             take(v[u].x, j), take(v[u].y, j + 1), take(v[u].z, j + 2), take(v[u].w, j + 3);
           }
         });
-    __syncthreads();
+    cta_sync();
     n = ncand;
     // Trim the candidates to (about) k before sorting: a radix select of the
     // k-th largest key over the shared-memory candidates (3 digits), then keep
@@ -435,17 +445,17 @@ __global__ void __launch_bounds__(kLT, 1)
       for (int p = 0; p < 3; ++p) {
         const int sh = shifts[p], nb = 1 << widths[p];
         for (int i = t; i < nb; i += kLT) hist[i] = 0u;
-        __syncthreads();
+        cta_sync();
         for (int i = t; i < n; i += kLT) {
           const unsigned u = ck[i];
           if ((u & pmask) == prefix) atomicAdd(&hist[(u >> sh) & (nb - 1)], 1u);
         }
-        __syncthreads();
+        cta_sync();
         pick_bucket(hist, nb, krem, sel, smi);
         prefix |= sel[0] << sh;
         pmask |= (unsigned)(nb - 1) << sh;
         krem -= (int)sel[1];
-        __syncthreads();
+        cta_sync();
       }
       const unsigned tau = prefix;
       constexpr int kPer = kFastCap / kLT;  // entries per thread (8)
@@ -458,7 +468,7 @@ __global__ void __launch_bounds__(kLT, 1)
         ii[q] = i < n ? ci[i] : 0;
       }
       if (t == 0) ncand = 0;
-      __syncthreads();
+      cta_sync();
 #pragma unroll
       for (int q = 0; q < kPer; ++q) {
         if (t + q * kLT < n && kk[q] >= tau) {
@@ -467,7 +477,7 @@ __global__ void __launch_bounds__(kLT, 1)
           ci[pos] = ii[q];
         }
       }
-      __syncthreads();
+      cta_sync();
       n = ncand;
     }
   } else {
@@ -483,7 +493,7 @@ __global__ void __launch_bounds__(kLT, 1)
     for (int p = 0; p < 3; ++p) {
       const int sh = shifts[p], nb = 1 << widths[p];
       for (int i = t; i < nb; i += kLT) hist[i] = 0u;
-      __syncthreads();
+      cta_sync();
       auto add = [&](float v) {
         const unsigned u = fkey(v);
         if ((u & pmask) == prefix) atomicAdd(&hist[(u >> sh) & (nb - 1)], 1u);
@@ -495,12 +505,12 @@ __global__ void __launch_bounds__(kLT, 1)
             for (int u = 0; u < U; ++u)
               if (u < cnt) add(v[u].x), add(v[u].y), add(v[u].z), add(v[u].w);
           });
-      __syncthreads();
+      cta_sync();
       pick_bucket(hist, nb, krem, sel, smi);
       prefix |= sel[0] << sh;
       pmask |= (unsigned)(nb - 1) << sh;
       krem -= (int)sel[1];
-      __syncthreads();
+      cta_sync();
     }
     const unsigned tau = prefix;
     const int need_eq = krem;
@@ -539,7 +549,7 @@ __global__ void __launch_bounds__(kLT, 1)
       gt_base += gtot;
       eq_base += etot;
     }
-    __syncthreads();
+    cta_sync();
     for (int i = t; i < k; i += kLT) {
       ck[i] = okey[i];
       ci[i] = oidx[i];
@@ -552,7 +562,7 @@ __global__ void __launch_bounds__(kLT, 1)
     ck[i] = 0u;
     ci[i] = 0x7fffffff;
   }
-  __syncthreads();
+  cta_sync();
   smem_bitonic(ck, ci, P);
   const double rd = 1.0 / (double)R;
   for (int r = t; r < k; r += kLT) {

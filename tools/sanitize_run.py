@@ -48,11 +48,29 @@ for knobs in ({"topk_threads": 32, "topk_u8": 1}, {"topk_threads": 32, "topk_pip
 x = dev(rng.standard_normal((3, 5000)).astype(np.float32))
 osmx.softmax_topk(x, 100)  # large k
 osmx.topk(x, 5000)
-x1 = dev(rng.standard_normal((1, 300000)).astype(np.float32))
-osmx.softmax_topk(x1, 5)  # one row: TMA-ring pieces + combine
+x = dev(rng.standard_normal((4, 20011)).astype(np.float32))
+osmx.softmax_topk(x, 1000)  # large k: two-pass shared-memory path with the candidate trim
+osmx.softmax_topk(dev(np.ones((2, 20011), dtype=np.float32)), 40)  # boundary bucket overflow: radix fallback
+_lib.config_set("large_fast", 0)
+osmx.softmax_topk(x, 100)  # large k: radix + CUB path
+_lib.config_set("large_fast", 1)
+big1 = rng.standard_normal((1, 300003)).astype(np.float32)
+x1 = dev(big1)[:, 1:]  # misaligned one row
+osmx.softmax_topk(x1, 5)  # one row: TMA ring over dynamic chunks + last-CTA merge
+osmx.topk(x1, 9)
+for cfg in (0, 2):
+    _lib.config_set("tma_cfg", cfg)
+    osmx.softmax_topk(x1, 5)
+_lib.config_set("tma_cfg", -1)
+_lib.config_set("split_cta", 2)
+osmx.softmax_topk(x1, 5)  # static TMA-ring pieces + combine launch
 _lib.config_set("split_cta", 0)
 osmx.softmax_topk(x1, 5)  # warp-piece split + combine
 osmx.topk(x1, 9)
 _lib.config_set("split_cta", -1)
+for V in (5623, 7500, 10000):  # staged layouts (2-warp groups up to 8K, <= 4 slots above)
+    xs = dev(rng.standard_normal((300, V)).astype(np.float32))
+    for alg in ("naive", "safe", "online"):
+        osmx.softmax(xs, alg=alg)
 torch.cuda.synchronize()
 print("sanitize run ok")
