@@ -523,7 +523,11 @@ cudaError_t run_staged_cfg(const float* x, long long ldx, float* y, long long ld
   for (int it = 0; it < 3; ++it) {  // ng and the header size depend on each other (C > 1)
     const size_t avail = (size_t)std::min(ring_kb * 1024, kStagedSmemMax) - staged_slots_off(ng, C);
     D = (int)std::min<size_t>(avail / slot, kStagedMaxD);
+#ifndef OSMX_TIMELINE  // the diagnostic build keeps the old layouts reachable (tools/runs/r2_bf.sh)
     if (D >= 5 && GW >= 4) ng = std::min(ng, D - 2);
+#else
+    if (false) {}
+#endif
     else if (D >= 2) ng = std::min(ng, D - 1);
   }
   // One-CTA rows above 8K elements: no deeper than NG + 1 = 4 slots (4000 x
