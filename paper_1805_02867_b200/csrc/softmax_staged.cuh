@@ -517,17 +517,15 @@ cudaError_t run_staged_cfg(const float* x, long long ldx, float* y, long long ld
   // while (4, 3), (5, 3) and every 1- and 2-warp-group layout (e.g. (7, 6)
   // at V = 3162, thousands of sweep launches) ran clean.  The cause is not
   // understood -- the slot protocol (one full / one empty mbarrier per slot,
-  // a group never more than one phase behind) checks out on paper -- so the
-  // defaults use 4-warp groups only with 3 groups (run_staged) and this
-  // guard covers the knobs.
+  // a group never more than one phase behind) checks out on paper, the
+  // sanitizers are clean, and non-.aligned named barriers did not cure it
+  // ((7, 6) still failed 1 run in 6 with the guard compiled out,
+  // tools/runs/r2_bf.sh) -- so the defaults use 4-warp groups only with 3
+  // groups (run_staged) and this guard covers the knobs.
   for (int it = 0; it < 3; ++it) {  // ng and the header size depend on each other (C > 1)
     const size_t avail = (size_t)std::min(ring_kb * 1024, kStagedSmemMax) - staged_slots_off(ng, C);
     D = (int)std::min<size_t>(avail / slot, kStagedMaxD);
-#ifndef OSMX_TIMELINE  // the diagnostic build keeps the old layouts reachable (tools/runs/r2_bf.sh)
     if (D >= 5 && GW >= 4) ng = std::min(ng, D - 2);
-#else
-    if (false) {}
-#endif
     else if (D >= 2) ng = std::min(ng, D - 1);
   }
   // One-CTA rows above 8K elements: no deeper than NG + 1 = 4 slots (4000 x
