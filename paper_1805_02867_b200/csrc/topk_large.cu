@@ -349,61 +349,34 @@ __global__ void __launch_bounds__(kLT, 1)
   if (t == 0) ncand = 0;
   cta_sync();
 
-  // pass A: statistics + top-11-bit histogram.  The first 16K elements are
-  // histogrammed in full; the k-th largest key among them is a lower bound
-  // of the row's k-th largest, so the rest of the row only counts keys in
-  // buckets >= that one (the suffix counts above it stay exact) -- most
-  // elements skip the contended shared-memory atomic.
-  unsigned hfloor = 0;
-  auto h = [&](float v) {
-    const unsigned b = fkey(v) >> 21;
-    if (b >= hfloor) atomicAdd(&hist[b], 1u);
-  };
-  constexpr long long kSampleQ = 4096;  // float4s in the fully counted prefix
-  const bool split_a = s.nvec > 2 * kSampleQ;
-  Seg sa = s, sb{};
-  if (split_a) {
-    sa.nvec = kSampleQ;
-    sa.tail = 0;
-    sa.n = s.head + 4 * kSampleQ;
-    sb = make_seg(xr + sa.n, V - sa.n);  // 16-byte aligned start
-  }
+  // pass A: statistics + top-11-bit histogram
+  auto h = [&](float v) { atomicAdd(&hist[fkey(v) >> 21], 1u); };
   float M = 0.0f, R = 1.0f;
   bool bad = false;
   if constexpr (MODE == 0) {
     L2Acc acc;
     float mn = -kNegInf;
-    auto part = [&](const Seg& sg) {
-      stream_seg<kLT, U, 2>(
-          sg, t,
-          [&](float v, long long) {
-            mn = fminf(mn, v);
-            acc.add1(v);
-            h(v);
-          },
-          [&](float4 (&v)[U], long long, int cnt) {
-            float bm = kNegInf, bn = -kNegInf;
+    stream_seg<kLT, U, 2>(
+        s, t,
+        [&](float v, long long) {
+          mn = fminf(mn, v);
+          acc.add1(v);
+          h(v);
+        },
+        [&](float4 (&v)[U], long long, int cnt) {
+          float bm = kNegInf, bn = -kNegInf;
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-              bm = fmaxf(bm, fmaxf(fmaxf(v[u].x, v[u].y), fmaxf(v[u].z, v[u].w)));
-              if (u < cnt) {
-                bn = fminf(bn, fminf(fminf(v[u].x, v[u].y), fminf(v[u].z, v[u].w)));
-                if ((fkey(fmaxf(fmaxf(v[u].x, v[u].y), fmaxf(v[u].z, v[u].w))) >> 21) >= hfloor)
-                  h(v[u].x), h(v[u].y), h(v[u].z), h(v[u].w);
-              }
+          for (int u = 0; u < U; ++u) {
+            bm = fmaxf(bm, fmaxf(fmaxf(v[u].x, v[u].y), fmaxf(v[u].z, v[u].w)));
+            if (u < cnt) {
+              bn = fminf(bn, fminf(fminf(v[u].x, v[u].y), fminf(v[u].z, v[u].w)));
+              h(v[u].x), h(v[u].y), h(v[u].z), h(v[u].w);
             }
-            mn = fminf(mn, bn);
-            acc.raise(bm);
-            acc.add_batch<U>(v);
-          });
-    };
-    part(sa);
-    if (split_a) {
-      cta_sync();
-      pick_bucket(hist, 2048, k, sel, smi);
-      hfloor = sel[0];
-      part(sb);
-    }
+          }
+          mn = fminf(mn, bn);
+          acc.raise(bm);
+          acc.add_batch<U>(v);
+        });
     const MD tot = md_cta_reduce<kLW>(acc.finish(), smf);
     mn = cta_min<kLW>(mn, smf);
     M = tot.m;
@@ -411,30 +384,20 @@ __global__ void __launch_bounds__(kLT, 1)
     bad = !(tot.d == tot.d) || !isfinite(M) || mn == kNegInf;
   } else {
     float chk = 0.0f;
-    auto part = [&](const Seg& sg) {
-      stream_seg<kLT, U, 2>(
-          sg, t,
-          [&](float v, long long) {
-            chk = fmaf(v, 0.0f, chk);
-            h(v);
-          },
-          [&](float4 (&v)[U], long long, int cnt) {
+    stream_seg<kLT, U, 2>(
+        s, t,
+        [&](float v, long long) {
+          chk = fmaf(v, 0.0f, chk);
+          h(v);
+        },
+        [&](float4 (&v)[U], long long, int cnt) {
 #pragma unroll
-            for (int u = 0; u < U; ++u)
-              if (u < cnt) {
-                chk = fmaf(v[u].x, 0.0f, fmaf(v[u].y, 0.0f, fmaf(v[u].z, 0.0f, fmaf(v[u].w, 0.0f, chk))));
-                if ((fkey(fmaxf(fmaxf(v[u].x, v[u].y), fmaxf(v[u].z, v[u].w))) >> 21) >= hfloor)
-                  h(v[u].x), h(v[u].y), h(v[u].z), h(v[u].w);
-              }
-          });
-    };
-    part(sa);
-    if (split_a) {
-      cta_sync();
-      pick_bucket(hist, 2048, k, sel, smi);
-      hfloor = sel[0];
-      part(sb);
-    }
+          for (int u = 0; u < U; ++u)
+            if (u < cnt) {
+              chk = fmaf(v[u].x, 0.0f, fmaf(v[u].y, 0.0f, fmaf(v[u].z, 0.0f, fmaf(v[u].w, 0.0f, chk))));
+              h(v[u].x), h(v[u].y), h(v[u].z), h(v[u].w);
+            }
+        });
     chk = cta_sum<kLW>(chk, smf);
     bad = !(chk == chk);
   }
