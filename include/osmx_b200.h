@@ -18,7 +18,11 @@
  *     osmx_workspace_bytes(...) bytes, zero-initialised once with
  *     osmx_workspace_init.  Non-finite input rows are reported through it
  *     (osmx_check_status), like the reference's non_finite_error
- *     (error.hpp:13-15); their outputs are unspecified.
+ *     (error.hpp:13-15); their outputs are unspecified.  A workspace also
+ *     carries the split paths' records, ticket counters and chunk counter
+ *     (reset by the kernels that use them): calls that may run concurrently
+ *     (different streams) need different workspaces; calls ordered on one
+ *     stream may share one.
  *   - Host-buffer entry points (suffix _host) mirror the reference's
  *     span-in / vector-out functions for a whole batch: they copy in, run,
  *     copy out and synchronise, and report non-finite input synchronously.
