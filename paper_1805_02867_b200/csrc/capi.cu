@@ -63,6 +63,28 @@ TuningScope::~TuningScope() {
 static std::atomic<unsigned long long> g_launches{0};
 void count_launch(int n) { g_launches.fetch_add((unsigned long long)n, std::memory_order_relaxed); }
 
+cudaError_t side_stream(cudaStream_t* side, cudaEvent_t* fork, cudaEvent_t* join) {
+  struct Side {
+    cudaStream_t s = nullptr;
+    cudaEvent_t f = nullptr, j = nullptr;
+  };
+  thread_local Side sides[64];  // per host thread and device: no sharing between concurrent callers
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  Side& sd = sides[dev];
+  if (!sd.s) {
+    cudaError_t e = cudaStreamCreateWithFlags(&sd.s, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&sd.f, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&sd.j, cudaEventDisableTiming);
+    if (e != cudaSuccess) return e;
+  }
+  *side = sd.s;
+  *fork = sd.f;
+  *join = sd.j;
+  return cudaSuccess;
+}
+
 int num_sms() {
   static int cache[64] = {0};
   int dev = 0;
@@ -416,6 +438,9 @@ osmx_status osmx_config_set(const char* key, int64_t value) {
   } else if (!strcmp(key, "tma")) {
     if (value < 0 || value > 2) return OSMX_ERR_INVALID_ARG;
     t.tma = (int)value;
+  } else if (!strcmp(key, "corun")) {
+    if (value < -1 || value > 99) return OSMX_ERR_INVALID_ARG;
+    t.corun = (int)value;
   } else if (!strcmp(key, "large_fast")) {
     if (value < 0 || value > 1) return OSMX_ERR_INVALID_ARG;
     t.large_fast = (int)value;
@@ -444,6 +469,7 @@ int64_t osmx_config_get(const char* key) {
   if (!strcmp(key, "tma")) return t.tma;
   if (!strcmp(key, "tma_cfg")) return t.tma_cfg;
   if (!strcmp(key, "large_fast")) return t.large_fast;
+  if (!strcmp(key, "corun")) return t.corun;
   if (!strcmp(key, "l2_prefetch")) return t.l2_prefetch;
   if (!strcmp(key, "topk_u8")) return t.topk_u8;
   if (!strcmp(key, "topk_pipe")) return t.topk_pipe;

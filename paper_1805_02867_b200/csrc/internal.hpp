@@ -57,6 +57,8 @@ struct Tuning {
   int topk_block = 0;           // threads per CTA of the one-wave warp-per-row top-K (0 auto = 32, 32, 128)
   int tma = 0;                  // TMA-ring top-K: 0 off (default: the warp-per-row
                                 // LDG kernel measures faster), 1 auto, 2 force
+  int corun = -1;               // 16-CTA-cluster rows: percent of rows for the cluster kernel, the rest
+                                // streamed concurrently on a side stream (-1 auto, 0 off)
   int large_fast = 1;           // k > 32: two-pass shared-memory path (1) or the radix + CUB path (0)
   int tma_cfg = -1;             // TMA-ring layout for fused k <= 5 (topk_tma.cu TmaCfg: -1 auto, 0, 1, 2)
 };
@@ -83,6 +85,9 @@ struct TuningScope {
 void count_launch(int n = 1);
 
 int num_sms();
+
+// A per-thread, per-device side stream and fork / join events (capi.cu).
+cudaError_t side_stream(cudaStream_t* side, cudaEvent_t* fork, cudaEvent_t* join);
 
 // True the first time it is called for (current device, fn): function
 // attributes (dynamic shared memory, cluster size) are per device context.

@@ -257,12 +257,12 @@ __global__ void __launch_bounds__(TPR > 256 ? TPR : 256)
 template <int BLOCK, int U, int ALG, int P1 = 0>
 __global__ void __launch_bounds__(BLOCK)
     k_softmax_stream(const float* __restrict__ x, long long ldx, float* __restrict__ y,
-                     long long ldy, long long rows, long long V, void* ws, int pf) {
+                     long long ldy, long long rows, long long V, void* ws, int pf, long long row0 = 0) {
   constexpr int NW = BLOCK / 32;
   __shared__ float smf[2 * NW];
   __shared__ double smd[NW];
   const int t = threadIdx.x;
-  for (long long row = blockIdx.x; row < rows; row += gridDim.x) {
+  for (long long row = row0 + blockIdx.x; row < rows; row += gridDim.x) {
     const Seg s = make_seg(x + row * ldx, V);
     float* yr = y + row * ldy;
     float mn = -kNegInf;
@@ -659,7 +659,7 @@ cudaError_t dispatch_resident(bool vec, const float* x, long long ldx, float* y,
 
 template <int ALG>
 cudaError_t run_stream(const float* x, long long ldx, float* y, long long ldy, long long rows,
-                       long long V, void* ws, cudaStream_t st) {
+                       long long V, void* ws, cudaStream_t st, long long row0 = 0) {
   int threads = osmx_host::tuning().stream_threads;
   const int pf = std::max(0, osmx_host::tuning().l2_prefetch);  // off unless forced (measured: mixed)
   // 1024-thread CTAs for long rows (4000 rows, same box, tools/runs/r2_aa.sh):
@@ -679,13 +679,13 @@ cudaError_t run_stream(const float* x, long long ldx, float* y, long long ldy, l
     osmx_host::count_launch();
     return cudaGetLastError();
   }
-  const long long grid = std::min<long long>(rows, 1LL << 30);
+  const long long grid = std::min<long long>(rows - row0, 1LL << 30);
   if (threads == 1024)
-    k_softmax_stream<1024, 4, ALG><<<(unsigned)grid, 1024, 0, st>>>(x, ldx, y, ldy, rows, V, ws, pf);
+    k_softmax_stream<1024, 4, ALG><<<(unsigned)grid, 1024, 0, st>>>(x, ldx, y, ldy, rows, V, ws, pf, row0);
   else if (threads == 512)
-    k_softmax_stream<512, 4, ALG><<<(unsigned)grid, 512, 0, st>>>(x, ldx, y, ldy, rows, V, ws, pf);
+    k_softmax_stream<512, 4, ALG><<<(unsigned)grid, 512, 0, st>>>(x, ldx, y, ldy, rows, V, ws, pf, row0);
   else
-    k_softmax_stream<256, 4, ALG><<<(unsigned)grid, 256, 0, st>>>(x, ldx, y, ldy, rows, V, ws, pf);
+    k_softmax_stream<256, 4, ALG><<<(unsigned)grid, 256, 0, st>>>(x, ldx, y, ldy, rows, V, ws, pf, row0);
   osmx_host::count_launch();
   return cudaGetLastError();
 }
@@ -753,6 +753,28 @@ cudaError_t launch_alg(const float* x, long long ldx, float* y, long long ldy, l
   }
   if (shape == osmx_host::kShapeResident && V + (vec ? 0 : 3) > 16384) shape = osmx_host::kShapeStream;
   if (shape == osmx_host::kShapeStaged || shape == osmx_host::kShapeCluster) {
+    // Rows that only a 16-CTA cluster holds: 7 clusters fill 112 of the 148
+    // SMs, so a share of the rows runs concurrently in the streaming kernel
+    // on a side stream (fork / join by events on the caller's stream; both
+    // flag bad rows with their global row index).
+    // Auto: online softmax only, 80% of the rows in clusters (4000 x 177828:
+    // 1.119 vs 1.178 ms, 196000: 1.255 vs 1.339; safe softmax measured
+    // slower co-run, 1.39 vs 1.33 -- tools/runs/r2_bj.sh).
+    const int co = tn.corun >= 0 ? tn.corun : (ALG == osmx_host::kOnline ? 80 : 0);
+    if (co > 0 && co < 100 && tn.cluster_size == 0 && V <= kClusterMaxV && V > kStagedMaxV &&
+        staged_cluster_size(V) == 16 && rows >= 2LL * osmx_host::num_sms()) {
+      const long long r1 = rows * co / 100;
+      cudaStream_t side;
+      cudaEvent_t fork, join;
+      cudaError_t e = osmx_host::side_stream(&side, &fork, &join);
+      if (e == cudaSuccess) e = cudaEventRecord(fork, st);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(side, fork, 0);
+      if (e == cudaSuccess) e = run_staged<ALG>(x, ldx, y, ldy, r1, V, ws, st);
+      if (e == cudaSuccess) e = run_stream<ALG>(x, ldx, y, ldy, rows, V, ws, side, r1);
+      if (e == cudaSuccess) e = cudaEventRecord(join, side);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(st, join, 0);
+      return e;
+    }
     if (V <= kClusterMaxV || osmx_host::tuning().cluster_size > 0) return run_staged<ALG>(x, ldx, y, ldy, rows, V, ws, st);
     shape = osmx_host::kShapeStream;
   }

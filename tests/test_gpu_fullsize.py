@@ -171,3 +171,34 @@ def test_config2_unfused_pipelines_full_rows(cuda, oracle_mod, V):
             if not np.array_equal(got[r], rz[r]):  # probability-rounding collisions only
                 assert np.allclose(np.sort(y[r][got[r]]), np.sort(y[r][rz[r]]), rtol=2.5e-7, atol=0), (alg, r)
         assert max_rel(vals[sample].cpu().numpy(), rv) <= TOL, alg
+
+
+@pytest.mark.parametrize("alg", ["online", "safe"])
+def test_cluster16_corun_rows(cuda, oracle_mod, alg):
+    """Rows only a 16-CTA cluster holds (166K < V <= 197K): a share of the
+    rows runs in the streaming kernel on a side stream, concurrently
+    (knob corun).  Sampled rows from both shares against the oracle, every
+    row sums to 1, and a non-finite row in the streamed share is reported
+    with its global index."""
+    import torch
+
+    from paper_1805_02867_b200 import _lib, osmx
+
+    rows, V = 4000, 177828
+    old = _lib.config_get("corun")
+    _lib.config_set("corun", 75)
+    try:
+        x = _normal((rows, V), 77)
+        y = osmx.softmax(x, alg=alg)
+        s = torch.cat([y[r0:r0 + 500].double().sum(dim=1) for r0 in range(0, rows, 500)])
+        assert float((s - 1.0).abs().max()) <= 1e-4
+        sample = [0, 2999, 3000, rows - 1]  # both sides of the 75% split
+        ry, st = oracle_mod.batch(f"{alg}_softmax", x[sample].cpu().numpy())
+        assert (st == 0).all()
+        assert max_rel(y[sample].cpu().numpy(), ry) <= TOL
+        x[3500, 123] = float("nan")
+        with pytest.raises(osmx.NonFiniteError) as ei:
+            osmx.softmax(x, alg=alg)
+        assert ei.value.row == 3500
+    finally:
+        _lib.config_set("corun", old)
