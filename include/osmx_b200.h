@@ -250,7 +250,14 @@ osmx_status osmx_diag_read_probe(const void* x, size_t bytes, float* sink, void*
  *   "topk_threads"   threads per row of the row top-K (0 auto, 32, 128, 256, 512)
  *   "topk_u8" / "topk_pipe" / "l2_prefetch" / "tma"   top-K row-kernel variants
  *   "split_cta"      top-K split records: -1 auto, 0 warp pieces, 1 CTA chunks,
- *                    2 TMA-ring CTA pieces
+ *                    2 TMA-ring CTA pieces, 3 one-launch grid-stride, 4 one row:
+ *                    TMA ring over dynamically claimed chunks (auto for one row)
+ *   "split_fuse"     TMA pieces: merge in the last piece CTA (1) or a combine launch (0)
+ *   "tma_cfg"        TMA-ring layout for fused k <= 5 (-1 auto, 0, 1, 2)
+ *   "topk_block"     threads per CTA of the one-wave warp-per-row top-K (0 auto, 32, 128)
+ *   "large_fast"     k > 32: two-pass shared-memory selection (1) or radix + CUB (0)
+ *   "corun"          online softmax, 16-CTA-cluster rows: percent of rows in clusters,
+ *                    the rest streamed on a side stream (-1 auto = 80, 0 off)
  *   "proj_bn"        fused projection vocabulary tile (0 auto, 128, 224, 256)
  *   "host_chunk_mb"  staging block of the host path (default 512)
  * Returns OSMX_ERR_INVALID_ARG for an unknown key or value. */
